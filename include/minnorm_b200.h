@@ -1,0 +1,195 @@
+/* minnorm_b200.h -- C ABI of the B200-native randomized minimal-norm hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch / Eigen
+ * types.  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).  A matrix is always the
+ * reference's layout: column-major complex<double> (interleaved re,im; 16 B),
+ * `A` is m x n with m < n, lda >= m (include/minnorm/types.hpp:10,
+ * SPEC.md:461).  A real float64 A (BASELINE config 5) is an extension.
+ *
+ * All functions return an MNB_* status; the message of the last failure on
+ * the calling thread is available from mnb_last_error().  The status codes
+ * map one-to-one onto the reference's exceptions
+ * (include/minnorm/errors.hpp:10-49) so a C++ shim can rethrow them and keep
+ * the CLI exit-code map of tools/minnorm_main.cpp:29-35.
+ */
+#ifndef MINNORM_B200_H
+#define MINNORM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define MNB_OK 0
+#define MNB_ERR_INVALID_ARGUMENT 1 /* std::invalid_argument (lsq.cpp:47-55, srft.cpp:97-98) */
+#define MNB_ERR_CONFIG 2           /* minnorm::ConfigError (errors.hpp:10-13)            */
+#define MNB_ERR_DIMENSION 3        /* minnorm::DimensionError (errors.hpp:16-19)         */
+#define MNB_ERR_RANK_DEFICIENCY 4  /* minnorm::RankDeficiencyError (errors.hpp:22-31)    */
+#define MNB_ERR_CUDA 5
+#define MNB_ERR_NCCL 6
+#define MNB_ERR_UNSUPPORTED 7      /* e.g. an FFT length this build has no kernel for   */
+#define MNB_ERR_OUT_OF_MEMORY 8
+#define MNB_ERR_INTERNAL 9
+
+/* ---- enums --------------------------------------------------------------- */
+#define MNB_C128 0 /* complex<double> */
+#define MNB_F64 1  /* double (real A; config 5) */
+#define MNB_HOST 0
+#define MNB_DEVICE 1
+#define MNB_WITHOUT_REPLACEMENT 0 /* RandomStream::Sampling (rng.hpp:18) */
+#define MNB_WITH_REPLACEMENT 1
+
+/* ---- errors / version ---------------------------------------------------- */
+const char* mnb_last_error(void);
+/* RankDeficiencyError::deficient_columns() of the last MNB_ERR_RANK_DEFICIENCY. */
+int64_t mnb_last_deficient_columns(void);
+const char* mnb_version(void);
+
+/* ---- context (one per GPU / per rank) ------------------------------------ */
+typedef struct mnb_context mnb_context;
+
+int mnb_context_create(int device, mnb_context** out);
+/* Column-sharded multi-GPU context: one process per GPU, NCCL communicator
+ * built from a 128-byte ncclUniqueId that rank 0 created with
+ * mnb_nccl_unique_id() and the launcher broadcast. */
+int mnb_nccl_unique_id(void* out128);
+int mnb_context_create_distributed(int device, int rank, int world_size, const void* nccl_unique_id,
+                                   mnb_context** out);
+void mnb_context_destroy(mnb_context* ctx);
+/* Run on the caller's CUDA stream (cudaStream_t) instead of the context's own. */
+int mnb_context_set_stream(mnb_context* ctx, void* cuda_stream);
+/* Column partition used by every multi-GPU entry point (pure host logic). */
+int mnb_shard_columns(int64_t n, int world_size, int rank, int64_t* col_begin, int64_t* col_count);
+
+/* The problem matrix A (ProblemInstance::A, include/minnorm/solver.hpp:14-24):
+ * this rank's column shard A[:, col_begin : col_begin+n_local], column-major
+ * with leading dimension lda >= m.  location MNB_DEVICE borrows the pointer
+ * (caller keeps it alive; requires lda == m), MNB_HOST copies it to the GPU. */
+int mnb_set_matrix(mnb_context* ctx, int dtype, int64_t m, int64_t n_global, int64_t col_begin,
+                   int64_t n_local, const void* A, int64_t lda, int location);
+
+/* ---- the solver (include/minnorm/solver.hpp:26-63) ------------------------ */
+typedef struct {
+    int64_t sketch_size;        /* SolverConfig::sketch_size; 0 = default 4m            */
+    double alpha;               /* SolverConfig::alpha (4.0)                             */
+    double epsilon;             /* SolverConfig::epsilon (1e-6)                          */
+    uint64_t seed;              /* SolverConfig::seed (42, rng.hpp:20)                   */
+    int32_t sampling;           /* SolverConfig::sampling (without replacement)          */
+    int32_t capture_c;          /* SolverConfig::capture_c                              */
+    int64_t lsq_max_iterations; /* SolverConfig::lsq_max_iterations (300)               */
+} mnb_solver_config;
+
+typedef struct {
+    double step_seconds[5];  /* SolveReport::step_seconds (device events per step)      */
+    double c_norm_ratio;     /* SolveReport::c_norm_ratio                               */
+    double residual_norm;    /* SolveReport::residual_norm = ||A x - b||                */
+    int64_t lsq_iterations;  /* SolveReport::lsq_iterations                             */
+    int32_t lsq_converged;   /* SolveReport::lsq_converged                              */
+    int32_t reserved0;
+    int64_t sketch_size;     /* SolveReport::sketch_size                                */
+    double lsq_tau;          /* SolveReport::lsq_tau                                    */
+    /* ---- extensions (not in the reference report) ---- */
+    double lsq_achieved_excess;  /* LsqSolution::achieved_excess (lsq.hpp:21)           */
+    double param_seconds;        /* host SRFT parameter generation (both operators)     */
+    double total_seconds;        /* whole solve, host wall clock                        */
+    double sketch_seconds[2];    /* device time of sketch S (step 1) and E (step 4)     */
+    double redistribute_seconds; /* all-to-all of A into row blocks (multi-GPU)         */
+    double qr_seconds[2];        /* device time of the two QRs                          */
+    double pcg_seconds;          /* device time of the CG loop                          */
+    double pcg_pass_ms_sum;      /* summed device time of the fused A(A^H w) passes     */
+    int64_t pcg_pass_launches;   /* number of fused-pass launches timed above           */
+    double sketch_kernel_ms[4];  /* summed device time per sketch kernel family:
+                                    [0] H stage 1, [1] H stage 2, [2] FFT pass A, [3] FFT pass B */
+    int64_t kernel_launches;     /* kernels this solve launched (own kernels only)      */
+    int64_t world_size;
+} mnb_solve_report;
+
+void mnb_solver_config_default(mnb_solver_config* cfg);
+
+/* solve_randomized(const ProblemInstance&, const SolverConfig&)
+ * (include/minnorm/solver.hpp:55; src/solver.cpp:50-128).
+ * b: m complex values; x_out: this rank's n_local complex values of x;
+ * c_out: optional (NULL) n_local values of the Step-3 vector c. */
+int mnb_solve_randomized(mnb_context* ctx, const void* b, int b_location, const mnb_solver_config* cfg,
+                         void* x_out, int x_location, void* c_out, mnb_solve_report* report);
+
+/* ---- the least-squares subsolver (include/minnorm/lsq.hpp:12-40) --------- */
+typedef struct {
+    int64_t sketch_size;    /* LsqConfig::sketch_size                                   */
+    double tau;             /* LsqConfig::tau                                           */
+    int64_t max_iterations; /* LsqConfig::max_iterations                               */
+    uint64_t stream_seed;   /* seed of LsqConfig::stream (RandomStream::seed())         */
+    int32_t sampling;       /* LsqConfig::sampling                                      */
+    int32_t reserved0;
+} mnb_lsq_config;
+
+typedef struct {
+    double achieved_excess; /* LsqSolution::achieved_excess */
+    int64_t iterations;     /* LsqSolution::iterations      */
+    int32_t converged;      /* LsqSolution::converged       */
+    int32_t reserved0;
+} mnb_lsq_solution;
+
+/* solve_least_squares(B, c, cfg) with B = A^H of the context matrix
+ * (src/lsq.cpp:43-113; the only B the solver ever passes, src/solver.cpp:112).
+ * c: n_local complex; y_out: m complex (host); residual_norms: optional array
+ * of max_iterations+1 doubles (LsqSolution::residual_norms). */
+int mnb_solve_least_squares(mnb_context* ctx, const void* c, int c_location, const mnb_lsq_config* cfg,
+                            void* y_out, double* residual_norms, mnb_lsq_solution* sol);
+
+/* ---- the SRFT operator (include/minnorm/srft.hpp:21-65) ------------------- */
+typedef struct mnb_srft mnb_srft;
+
+/* build_srft(l, n, RandomStream(stream_seed), sampling) (src/srft.cpp:95-113):
+ * host-side, bit-identical parameters to the reference RandomStream. */
+int mnb_srft_build(int64_t l, int64_t n, uint64_t stream_seed, int sampling, mnb_srft** out);
+/* An operator from explicit fields (tests: trivial / hand-built operators;
+ * tests/test_support.hpp:110-126).  Complex arrays interleaved. */
+int mnb_srft_from_fields(int64_t l, int64_t n, int sampling, const double* d, const int64_t* sample,
+                         const double* theta, const double* theta_tilde, const int64_t* perm,
+                         const int64_t* perm_tilde, const double* zeta, const double* zeta_tilde,
+                         mnb_srft** out);
+void mnb_srft_destroy(mnb_srft* op);
+/* Copy a parameter field out (field ids as MNB_FIELD_*). */
+#define MNB_FIELD_D 0
+#define MNB_FIELD_ZETA 1
+#define MNB_FIELD_ZETA_TILDE 2
+#define MNB_FIELD_THETA 3
+#define MNB_FIELD_THETA_TILDE 4
+#define MNB_FIELD_COS_THETA 5
+#define MNB_FIELD_SIN_THETA 6
+#define MNB_FIELD_COS_THETA_TILDE 7
+#define MNB_FIELD_SIN_THETA_TILDE 8
+#define MNB_FIELD_PERM 9
+#define MNB_FIELD_PERM_TILDE 10
+#define MNB_FIELD_SAMPLE 11
+int mnb_srft_get_field(const mnb_srft* op, int field, void* out);
+int mnb_srft_dims(const mnb_srft* op, int64_t* l, int64_t* n);
+
+/* SrftOperator::apply_h / apply / apply_adjoint (src/srft.cpp:115-145) on the GPU,
+ * host vectors in and out (tests and single-vector use). */
+int mnb_srft_apply_h(mnb_context* ctx, const mnb_srft* op, const void* x, void* y);
+int mnb_srft_apply(mnb_context* ctx, const mnb_srft* op, const void* x, void* y);
+int mnb_srft_apply_adjoint(mnb_context* ctx, const mnb_srft* op, const void* v, void* y);
+/* SrftOperator::apply_to_columns(B) with B = A^H of the context matrix
+ * (src/srft.cpp:147-153 as called at src/solver.cpp:81 and src/lsq.cpp:56):
+ * out = l x m column-major (complex), on host or device.  Multi-GPU: includes
+ * the all-to-all into row blocks; every rank receives the full sketch. */
+int mnb_srft_apply_to_columns(mnb_context* ctx, const mnb_srft* op, void* out, int out_location);
+
+/* Unitary DFT (src/fft.cpp:90-110; include/minnorm/fft.hpp:12) of a host vector. */
+int mnb_dft(mnb_context* ctx, int64_t n, void* x, int inverse);
+
+/* ---- benchmarking hooks (device-resident, CUDA-event timed) -------------- */
+/* Times `reps` launches of the fused PCG pass s = A(A^H w), qq = ||A^H w||^2
+ * over the context matrix; returns the mean per-launch milliseconds. */
+int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MINNORM_B200_H */

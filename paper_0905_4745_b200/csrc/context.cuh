@@ -1,0 +1,150 @@
+// Per-GPU context: stream, library handles, communicator, the (sharded)
+// problem matrix, cached FFT plans and grow-only workspaces.
+#pragma once
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+#include "host_srft.hpp"
+#include "kernels.cuh"
+#include "pcg.cuh"
+
+namespace mnb {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    void* ensure(size_t need) {
+        if (need > bytes) {
+            if (p) MNB_CUDA(cudaFree(p));
+            p = nullptr;
+            bytes = 0;
+            MNB_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return p;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() { if (p) cudaFreeHost(p); }
+    void* ensure(size_t need) {
+        if (need > bytes) {
+            if (p) MNB_CUDA(cudaFreeHost(p));
+            p = nullptr;
+            bytes = 0;
+            MNB_CUDA(cudaHostAlloc(&p, need, cudaHostAllocDefault));
+            bytes = need;
+        }
+        return p;
+    }
+};
+
+// Device-side FFT plan for one length n (four-step or single pass).
+struct FftLenPlan {
+    int N = 1, E = 1, nradix = 0, radix[10] = {0};
+    bool direct = false;
+    DevBuf tw;  // w_N^q
+};
+struct FftPlan {
+    int64_t n = 0, n1 = 1, n2 = 1;  // n = n1 * n2 ; pass A length n2 (batches n1), pass B length n1
+    bool single = true;
+    FftLenPlan A, B;                 // single: only A (N = n)
+    DevBuf tw4_hi, tw4_lo;
+    int tw4_shift = 0;
+};
+
+// Device copy of one operator's parameter blob (layout of SrftHost).
+struct SrftDev {
+    const SrftHost* host = nullptr;
+    DevBuf blob;
+    DevBuf dups;
+    int64_t ndups = 0;
+    template <class T> const T* at(size_t off) const { return reinterpret_cast<const T*>(blob.as<unsigned char>() + off); }
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    cublasHandle_t cublas = nullptr;
+    cusolverDnHandle_t cusolver = nullptr;
+    cusolverDnParams_t cusolver_params = nullptr;
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+
+    // problem matrix (this rank's column shard)
+    int dtype = MNB_C128;
+    int64_t m = 0, n_global = 0, col_begin = 0, n_local = 0;
+    const void* A = nullptr;
+    DevBuf A_own;
+
+    std::map<int64_t, std::unique_ptr<FftPlan>> fft_plans;
+    int64_t launches = 0;  // own kernels launched (for reporting)
+
+    // workspaces
+    DevBuf ws_x1, ws_x2, ws_slab, ws_pack;
+    DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info;
+    DevBuf Rinv, Rinv_rows;
+    DevBuf vec_m[8], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, state, resid, scratch;
+    DevBuf rhs, flag, out_c;
+    int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
+    PinnedBuf pin_params[2], pin_small;
+    std::vector<cudaEvent_t> events;
+    std::vector<unsigned char> host_work;  // cuSOLVER host workspace (kept alive across async calls)
+
+    ~Context();
+    cudaEvent_t event(size_t i);
+    FftPlan& fft_plan(int64_t n);
+    size_t esz() const { return dtype == MNB_F64 ? 8 : 16; }
+};
+
+// ---- SRFT on the GPU (srft_gpu.cu) ----
+void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev);
+// T * conj(rows [row0,row0+rows) of a column-major block) -> out[slot + (out_row0 + r) * ldo]
+void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real, int64_t lda, int64_t row0,
+                  int64_t rows, double2* out, int64_t ldo, int64_t out_row0, double* kernel_ms);
+// Full sketch of the context matrix (multi-GPU: all-to-all + allgather): out l x m col-major (device).
+void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel_ms, double* redistribute_s);
+// T^* v for one device vector v (l) -> y (n, device).
+void srft_adjoint_vec(Context& ctx, const SrftDev& op, const double2* v, double2* y);
+// T x / H x for one device vector.
+void srft_apply_vec(Context& ctx, const SrftDev& op, const double2* x, double2* y, bool h_only);
+void dft_vec(Context& ctx, int64_t n, double2* x, bool inverse);
+
+// ---- solver (solver.cu) ----
+struct LsqResult {
+    int64_t iterations = 0;
+    bool converged = false;
+    double achieved_excess = 0.0;
+    double rr0 = 0.0;
+    std::vector<double> residual_norms;
+    double pass_ms = 0.0;
+    int64_t pass_launches = 0;
+    double pcg_seconds = 0.0;
+};
+void sync(Context& ctx);
+void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
+                      double2* c_dev, mnb_solve_report& rep);
+void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
+                         double* residual_norms, mnb_lsq_solution& sol);
+double bench_pcg_pass(Context& ctx, int reps);
+
+}  // namespace mnb

@@ -1,0 +1,264 @@
+// Host parameter generation for the SRFT (bit-identical to the reference's
+// seeded draws; see host_srft.hpp).  Compiled by the host C++ compiler with
+// -ffp-contract=off so every draw rounds exactly like src/rng.cpp.
+#include "host_srft.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "common_host.hpp"
+
+namespace mnb {
+
+namespace {
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;  // 2.0 * std::numbers::pi, folded exactly
+inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+inline uint64_t mix(uint64_t z) {  // splitmix64 finalizer
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+// Substream tags of build_srft (src/srft.cpp:13-22).
+enum : uint64_t { kD = 1, kSample = 2, kTheta = 3, kThetaTilde = 4, kPerm = 5, kPermTilde = 6,
+                  kZeta = 7, kZetaTilde = 8 };
+// Scan halo: stop once the carried product of |sin| drops below 2^-70.
+constexpr double kHaloThreshold = 0x1.0p-70;
+}  // namespace
+
+RandomStream::RandomStream(uint64_t seed) : seed_(seed) {
+    uint64_t sm = seed;
+    for (auto& w : s_) { sm += kGolden; w = mix(sm); }
+}
+uint64_t RandomStream::derive_seed(uint64_t tag) const {
+    return mix(mix(seed_ + kGolden) ^ mix(tag + 2 * kGolden));
+}
+uint64_t RandomStream::next_u64() {
+    const uint64_t r = rotl(s_[0] + s_[3], 23) + s_[0];
+    const uint64_t t = s_[1] << 17;
+    s_[2] ^= s_[0];
+    s_[3] ^= s_[1];
+    s_[1] ^= s_[2];
+    s_[0] ^= s_[3];
+    s_[2] ^= t;
+    s_[3] = rotl(s_[3], 45);
+    return r;
+}
+double RandomStream::uniform_angle() { return kTwoPi * uniform01(); }
+void RandomStream::unit_circle(double* z) {
+    const double phi = uniform_angle();
+    ::sincos(phi, &z[1], &z[0]);
+}
+void RandomStream::complex_gaussian(double* z) {
+    const double u = 1.0 - uniform01();
+    const double r = std::sqrt(-std::log(u));
+    const double phi = uniform_angle();
+    double s, c;
+    ::sincos(phi, &s, &c);
+    z[0] = r * c;
+    z[1] = r * s;
+}
+uint64_t RandomStream::uniform_below(uint64_t bound) {
+    if (bound == 0) throw Error(MNB_ERR_INVALID_ARGUMENT, "uniform_below: bound must be positive");
+    const uint64_t threshold = (0 - bound) % bound;
+    for (;;) {
+        const uint64_t r = next_u64();
+        if (r >= threshold) return r % bound;
+    }
+}
+void RandomStream::permutation(int32_t* p, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) p[i] = int32_t(i);
+    for (int64_t i = n; i > 1; --i) {
+        const int64_t j = int64_t(uniform_below(uint64_t(i)));
+        std::swap(p[i - 1], p[j]);
+    }
+}
+void RandomStream::sample_indices(int64_t* out, int64_t l, int64_t n, bool without) {
+    if (l < 1 || n < 1) throw Error(MNB_ERR_INVALID_ARGUMENT, "sample_indices: l and n must be positive");
+    if (without) {
+        if (l > n)
+            throw Error(MNB_ERR_INVALID_ARGUMENT, "sample_indices: l > n with without-replacement sampling");
+        std::vector<int32_t> pool(static_cast<size_t>(n));
+        std::iota(pool.begin(), pool.end(), 0);
+        for (int64_t i = 0; i < l; ++i) {
+            const int64_t j = i + int64_t(uniform_below(uint64_t(n - i)));
+            std::swap(pool[size_t(i)], pool[size_t(j)]);
+        }
+        for (int64_t i = 0; i < l; ++i) out[i] = pool[size_t(i)];
+        return;
+    }
+    for (int64_t i = 0; i < l; ++i) out[i] = int64_t(uniform_below(uint64_t(n)));
+}
+
+ChainChunks chain_chunks(int64_t n) {
+    ChainChunks c;
+    int64_t chunk = 1024;
+    while (chunk > 64 && n / chunk < 16) chunk >>= 1;
+    c.chunk = chunk;
+    c.nchunks = (n + chunk - 1) / chunk;
+    return c;
+}
+
+void SrftHost::layout() {
+    ch = chain_chunks(n);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~size_t(255); return o; };
+    const size_t nn = size_t(n), ll = size_t(l);
+    off_d = take(16 * nn);
+    off_zeta = take(16 * nn);
+    off_zeta_tilde = take(16 * nn);
+    off_cssn = take(16 * nn);
+    off_cssn_tilde = take(16 * nn);
+    off_perm = take(4 * nn);
+    off_perm_tilde = take(4 * nn);
+    off_sel = take(4 * nn);
+    off_halo = take(4 * 4 * size_t(ch.nchunks));
+    off_sample = take(4 * ll);
+    device_bytes = off;
+    off_theta = take(8 * nn);
+    off_theta_tilde = take(8 * nn);
+    off_sample64 = take(8 * ll);
+    total_bytes = off;
+}
+
+// Halo starts: per chunk, where the chunked scan may initialise its carry so
+// that the neglected contribution is below kHaloThreshold (the carry of the
+// chain recurrence decays by |sin(theta_j)| per step).
+static void chain_halos(const double* cssn, int64_t n, const ChainChunks& ch, int32_t* fwd, int32_t* adj) {
+    for (int64_t c = 0; c < ch.nchunks; ++c) {
+        const int64_t i0 = c * ch.chunk, i1 = std::min(n, i0 + ch.chunk);
+        // forward chain: carry flows from high to low indices
+        int64_t t = i1;
+        if (i1 >= n) t = n - 1;
+        else {
+            double p = 1.0;
+            while (t < n - 1 && p > kHaloThreshold) { p *= std::fabs(cssn[2 * t + 1]); ++t; }
+        }
+        fwd[c] = int32_t(t);
+        // adjoint chain: carry flows from low to high indices
+        int64_t s = i0;
+        double p = 1.0;
+        while (s > 0 && p > kHaloThreshold) { --s; p *= std::fabs(cssn[2 * s + 1]); }
+        adj[c] = int32_t(s);
+    }
+}
+
+void SrftHost::derive() {
+    const int64_t nc = ch.nchunks;
+    int32_t* halo = at<int32_t>(off_halo);
+    chain_halos(at<double>(off_cssn), n, ch, halo, halo + 2 * nc);
+    chain_halos(at<double>(off_cssn_tilde), n, ch, halo + nc, halo + 3 * nc);
+    // selection map: frequency -> first output slot; duplicates listed.
+    int32_t* sel = at<int32_t>(off_sel);
+    std::fill(sel, sel + n, -1);
+    const int64_t* s64 = at<int64_t>(off_sample64);
+    int32_t* s32 = at<int32_t>(off_sample);
+    dups.clear();
+    for (int64_t j = 0; j < l; ++j) {
+        const int64_t f = s64[j];
+        s32[j] = int32_t(f);
+        if (sel[f] < 0) sel[f] = int32_t(j);
+        else { dups.push_back(int32_t(j)); dups.push_back(sel[f]); }
+    }
+    // max multiplicity (src/lsq.cpp:31-39)
+    max_mult = 1;
+    if (!dups.empty()) {
+        std::vector<int64_t> s(s64, s64 + l);
+        std::sort(s.begin(), s.end());
+        int64_t run = 1;
+        for (size_t i = 1; i < s.size(); ++i) {
+            run = (s[i] == s[i - 1]) ? run + 1 : 1;
+            max_mult = std::max(max_mult, run);
+        }
+    }
+}
+
+namespace {
+// Run fn(i) for i in [0, count) on up to `threads` workers.
+template <class F>
+void parallel_for(int64_t count, int threads, F&& fn) {
+    if (count <= 0) return;
+    threads = int(std::min<int64_t>(threads, count));
+    if (threads <= 1) { for (int64_t i = 0; i < count; ++i) fn(i); return; }
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    pool.reserve(size_t(threads));
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&] {
+            for (int64_t i; (i = next.fetch_add(1)) < count;) fn(i);
+        });
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
+void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, int sampling,
+                     const BlobAlloc& alloc, const BlobFree& release, int threads) {
+    // src/srft.cpp:97-98
+    if (n < 2) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: n must be at least 2");
+    if (l < 1 || l > n) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: need 1 <= l <= n");
+    if (n >= (int64_t(1) << 31)) throw Error(MNB_ERR_UNSUPPORTED, "build_srft: n must be below 2^31");
+    if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
+    op.n = n;
+    op.l = l;
+    op.sampling = sampling;
+    op.layout();
+    op.blob = alloc(op.total_bytes);
+    op.release = release;
+    const RandomStream stream(stream_seed);
+    const bool without = sampling == MNB_WITHOUT_REPLACEMENT;
+
+    // Phase 1: the eight tagged substreams, concurrently.  Unit-circle draws
+    // stash the angle phi in the real slot; phase 2 turns it into e^{i phi}.
+    double* d = op.at<double>(op.off_d);
+    double* zeta = op.at<double>(op.off_zeta);
+    double* zeta_t = op.at<double>(op.off_zeta_tilde);
+    double* theta = op.at<double>(op.off_theta);
+    double* theta_t = op.at<double>(op.off_theta_tilde);
+    auto angles_into = [&](RandomStream s, double* out, int64_t count, int64_t stride) {
+        for (int64_t i = 0; i < count; ++i) out[i * stride] = s.uniform_angle();
+    };
+    parallel_for(8, threads, [&](int64_t task) {
+        switch (task) {
+            case 0: angles_into(stream.substream(kD), d, n, 2); break;
+            case 1: {
+                RandomStream s = stream.substream(kSample);
+                s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
+            } break;
+            case 2: angles_into(stream.substream(kTheta), theta, n - 1, 1); break;
+            case 3: angles_into(stream.substream(kThetaTilde), theta_t, n - 1, 1); break;
+            case 4: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
+            case 5: { RandomStream s = stream.substream(kPermTilde); s.permutation(op.at<int32_t>(op.off_perm_tilde), n); } break;
+            case 6: angles_into(stream.substream(kZeta), zeta, n, 2); break;
+            case 7: angles_into(stream.substream(kZetaTilde), zeta_t, n, 2); break;
+        }
+    });
+    // Phase 2: sincos of all angles (unit_circle, rng.cpp:62-65; finalize, srft.cpp:80-93).
+    double* cssn = op.at<double>(op.off_cssn);
+    double* cssn_t = op.at<double>(op.off_cssn_tilde);
+    const int64_t blk = 1 << 15;
+    const int64_t nb = (n + blk - 1) / blk;
+    parallel_for(5 * nb, threads, [&](int64_t task) {
+        const int64_t which = task / nb, b0 = (task % nb) * blk;
+        if (which < 3) {
+            double* z = which == 0 ? d : which == 1 ? zeta : zeta_t;
+            const int64_t e = std::min(n, b0 + blk);
+            for (int64_t i = b0; i < e; ++i) {
+                const double phi = z[2 * i];
+                ::sincos(phi, &z[2 * i + 1], &z[2 * i]);
+            }
+        } else {
+            const double* th = which == 3 ? theta : theta_t;
+            double* cs = which == 3 ? cssn : cssn_t;
+            const int64_t e = std::min(n - 1, b0 + blk);
+            for (int64_t i = b0; i < e; ++i) ::sincos(th[i], &cs[2 * i + 1], &cs[2 * i]);
+            if (e == n - 1 && b0 <= n - 1) { cs[2 * (n - 1)] = 1.0; cs[2 * (n - 1) + 1] = 0.0; }
+        }
+    });
+    op.derive();
+}
+
+}  // namespace mnb

@@ -1,0 +1,346 @@
+// Batched FP64 FFT passes over rows of a column-major block (sm_100a).
+//
+// Replaces the reference's per-row radix-2 / Bluestein Fft::forward
+// (src/fft.cpp:65-97) inside the SRFT sketch.  A length-n transform is a
+// four-step n = n1*n2 (two launches: pass A = length-n2 DFTs over the
+// stride-n1 sub-sequences with the w_n^{f2 k1} twiddle fused into the
+// epilogue, pass B = length-n1 DFTs whose epilogue keeps only the l sampled
+// frequencies, src/srft.cpp:131), or a single launch for n <= 2048.
+//
+// One CTA = Rb rows x one length-N sub-transform.  Each thread keeps E
+// elements in registers; a pass of radix R (R | E) is E/R register
+// butterflies; passes exchange data through shared memory in place (all
+// reads, barrier, all writes).  Mixed-radix Stockham ordering, so the output
+// is in natural order with no bit reversal.  Radices 16, 8, 4, 3, 2.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mnb {
+
+namespace {
+
+template <bool INV>
+__device__ __forceinline__ double2 mul_mi(double2 a) {  // a * (-i) forward, a * (+i) inverse
+    return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+    const double2 t = a;
+    a = c_add(t, b);
+    b = c_sub(t, b);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+    const double2 t0 = c_add(x0, x2), t1 = c_sub(x0, x2);
+    const double2 t2 = c_add(x1, x3), t3 = mul_mi<INV>(c_sub(x1, x3));
+    x0 = c_add(t0, t2);
+    x2 = c_sub(t0, t2);
+    x1 = c_add(t1, t3);
+    x3 = c_sub(t1, t3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft3(double2& x0, double2& x1, double2& x2) {
+    constexpr double h = 0.86602540378443864676;  // sqrt(3)/2
+    const double2 t1 = c_add(x1, x2);
+    const double2 t2 = make_double2(x0.x - 0.5 * t1.x, x0.y - 0.5 * t1.y);
+    const double2 d = c_sub(x1, x2);
+    const double2 t3 = mul_mi<INV>(make_double2(h * d.x, h * d.y));
+    x0 = c_add(x0, t1);
+    x1 = c_add(t2, t3);
+    x2 = c_sub(t2, t3);
+}
+
+template <bool INV>
+__device__ __forceinline__ double2 w8mul(double2 a, int k) {  // a * w8^k, k in {1,2,3}
+    constexpr double r = 0.70710678118654752440;
+    if (k == 2) return mul_mi<INV>(a);
+    // w8^1 = (1 - i)/sqrt2 (fwd), w8^3 = (-1 - i)/sqrt2 (fwd)
+    const double2 m = mul_mi<INV>(a);  // a*(-i)
+    if (k == 1) return make_double2(r * (a.x + m.x), r * (a.y + m.y));
+    return make_double2(r * (m.x - a.x), r * (m.y - a.y));
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(double2* x) {
+    // even/odd split: E = DFT4(x0,x2,x4,x6), O = DFT4(x1,x3,x5,x7)
+    dft4<INV>(x[0], x[2], x[4], x[6]);
+    dft4<INV>(x[1], x[3], x[5], x[7]);
+    double2 o1 = w8mul<INV>(x[3], 1), o2 = w8mul<INV>(x[5], 2), o3 = w8mul<INV>(x[7], 3);
+    const double2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6], o0 = x[1];
+    x[0] = c_add(e0, o0); x[4] = c_sub(e0, o0);
+    x[1] = c_add(e1, o1); x[5] = c_sub(e1, o1);
+    x[2] = c_add(e2, o2); x[6] = c_sub(e2, o2);
+    x[3] = c_add(e3, o3); x[7] = c_sub(e3, o3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft16(double2* x) {
+    // n = n2 + 4 n1, k = k1 + 4 k2:  y[k1+4k2] = sum_n2 w4^{n2 k2} w16^{n2 k1} sum_n1 w4^{n1 k1} x[n2+4n1]
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(x[n2], x[n2 + 4], x[n2 + 8], x[n2 + 12]);
+    // after: x[n2 + 4 k1] = A[n2][k1]; twiddle by w16^{n2 k1}
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, r = 0.70710678118654752440;
+    const double sg = INV ? 1.0 : -1.0;
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) {
+            const int e = n2 * k1;  // 1..9
+            double wc, ws;
+            switch (e) {
+                case 1: wc = c1; ws = s1; break;
+                case 2: wc = r; ws = r; break;
+                case 3: wc = s1; ws = c1; break;
+                case 4: wc = 0.0; ws = 1.0; break;
+                case 6: wc = -r; ws = r; break;
+                case 9: wc = -c1; ws = -s1; break;
+                default: wc = 1.0; ws = 0.0; break;
+            }
+            const double2 w = make_double2(wc, sg * ws);
+            x[n2 + 4 * k1] = c_mul(x[n2 + 4 * k1], w);
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(x[4 * k1], x[4 * k1 + 1], x[4 * k1 + 2], x[4 * k1 + 3]);
+    // now x[4 k1 + k2] = y[k1 + 4 k2]: transpose 4x4 in registers
+    double2 t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = x[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft_r(double2* x) {
+    if constexpr (R == 2) dft2<INV>(x[0], x[1]);
+    else if constexpr (R == 3) dft3<INV>(x[0], x[1], x[2]);
+    else if constexpr (R == 4) dft4<INV>(x[0], x[1], x[2], x[3]);
+    else if constexpr (R == 8) dft8<INV>(x);
+    else if constexpr (R == 16) dft16<INV>(x);
+}
+
+__device__ __forceinline__ double2 tw_at(const double2* __restrict__ tw, int64_t q, bool inv) {
+    double2 w = __ldg(tw + q);
+    if (inv) w.y = -w.y;
+    return w;
+}
+
+// Load phase helper: first pass reads global, later passes read shared.
+template <int Rb, int E, bool INV>
+struct FftCta {
+    const FftPassArgs& a;
+    double2* sm;
+    int r, u, U;
+    int64_t row, b;
+    bool row_ok;
+
+    __device__ __forceinline__ double2 gload(int idx) const {
+        if (!row_ok) return make_double2(0.0, 0.0);
+        const int64_t col = b * a.in_bstride + int64_t(idx) * a.in_istride;
+        return __ldg(a.in + (a.in_row0 + row) + col * a.ld_in);
+    }
+
+    __device__ __forceinline__ void gstore(int f, double2 v) const {
+        if (!row_ok) return;
+        if (a.mode == FFT_OUT_TWIDDLE) {
+            const int64_t e = (int64_t(f) * b) % a.n_total;
+            double2 w = c_mul(__ldg(a.tw4_hi + (e >> a.tw4_shift)), __ldg(a.tw4_lo + (e & ((int64_t(1) << a.tw4_shift) - 1))));
+            if (INV) w.y = -w.y;
+            v = c_mul(v, w);
+            const int64_t col = int64_t(f) * a.out_fstride + b * a.out_bstride;
+            a.out[(a.out_row0 + row) + col * a.ld_out] = v;
+        } else if (a.mode == FFT_OUT_SELECT) {
+            const int64_t F = b + a.nb * int64_t(f);
+            const int slot = __ldg(a.sel + F);
+            if (slot >= 0) a.out[int64_t(slot) + (a.out_row0 + row) * a.ld_out] = c_scale(v, a.scale);
+        } else {
+            const int64_t col = b + a.nb * int64_t(f);
+            a.out[(a.out_row0 + row) + col * a.ld_out] = c_scale(v, a.scale);
+        }
+    }
+
+    template <int R>
+    __device__ __forceinline__ void pass(double2 (&v)[E], int Ns, bool first, bool last) {
+        constexpr int B = E / R;  // butterflies per thread
+        const int N = a.N;
+        const int NR = N / R;
+        // read
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+            const int j = u + s * U;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int idx = j + q * NR;
+                v[s * R + q] = first ? gload(idx) : sm[idx * Rb + r];
+            }
+        }
+        // twiddle + butterfly
+        const int stride = N / (Ns * R);
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+            const int j = u + s * U;
+            const int k = j % Ns;
+            if (k != 0) {
+#pragma unroll
+                for (int q = 1; q < R; ++q) v[s * R + q] = c_mul(v[s * R + q], tw_at(a.tw, int64_t(k) * q * stride, INV));
+            }
+            dft_r<R, INV>(&v[s * R]);
+        }
+        if (!first) __syncthreads();  // all in-place reads done before any write
+        // write
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+            const int j = u + s * U;
+            const int k = j % Ns;
+            const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int o = idxD + q * Ns;
+                if (last) gstore(o, v[s * R + q]);
+                else sm[o * Rb + r] = v[s * R + q];
+            }
+        }
+        if (!last) __syncthreads();
+    }
+};
+
+template <int Rb, int E, bool INV>
+__global__ void __launch_bounds__(1024) fft_pass_kernel(const FftPassArgs a) {
+    extern __shared__ double2 sm[];
+    FftCta<Rb, E, INV> cta{a, sm, int(threadIdx.x % Rb), int(threadIdx.x / Rb), a.N / E, 0, 0, false};
+    cta.row = int64_t(blockIdx.x) * Rb + cta.r;
+    cta.row_ok = cta.row < a.rows;
+    cta.b = blockIdx.y;
+    double2 v[E];
+    int Ns = 1;
+    for (int p = 0; p < a.nradix; ++p) {
+        const int R = a.radix[p];
+        const bool first = p == 0, last = p == a.nradix - 1;
+        switch (R) {
+            case 2: if constexpr (E % 2 == 0) cta.template pass<2>(v, Ns, first, last); break;
+            case 3: if constexpr (E % 3 == 0) cta.template pass<3>(v, Ns, first, last); break;
+            case 4: if constexpr (E % 4 == 0) cta.template pass<4>(v, Ns, first, last); break;
+            case 8: if constexpr (E % 8 == 0) cta.template pass<8>(v, Ns, first, last); break;
+            case 16: if constexpr (E % 16 == 0) cta.template pass<16>(v, Ns, first, last); break;
+            default: break;
+        }
+        Ns *= R;
+    }
+}
+
+// N == 1: the transform is the identity; only the epilogue (twiddle/select) runs.
+template <bool INV>
+__global__ void fft_len1_kernel(const FftPassArgs a) {
+    const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= a.rows) return;
+    FftCta<1, 1, INV> cta{a, nullptr, 0, 0, 1, row, int64_t(blockIdx.y), true};
+    cta.gstore(0, cta.gload(0));
+}
+
+// O(N^2) direct DFT (any N <= 4096): one thread per (row, frequency).
+template <bool INV>
+__global__ void dft_direct_kernel(const FftPassArgs a) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t row = blockIdx.z;
+    if (f >= a.N) return;
+    FftCta<1, 1, INV> cta{a, nullptr, 0, 0, 1, row, int64_t(blockIdx.y), true};
+    double2 acc = make_double2(0.0, 0.0);
+    int64_t q = 0;
+    for (int k = 0; k < a.N; ++k) {
+        acc = c_add(acc, c_mul(cta.gload(k), tw_at(a.tw, q, INV)));
+        q += f;
+        if (q >= a.N) q -= a.N;
+    }
+    cta.gstore(f, acc);
+}
+
+template <int Rb, int E>
+void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
+    const int threads = Rb * a.N / E;
+    const size_t smem = size_t(Rb) * a.N * sizeof(double2);
+    dim3 grid(ceil_div(a.rows, Rb), unsigned(a.batches));
+    if (a.inverse) {
+        auto k = fft_pass_kernel<Rb, E, true>;
+        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k<<<grid, threads, smem, stream>>>(a);
+    } else {
+        auto k = fft_pass_kernel<Rb, E, false>;
+        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k<<<grid, threads, smem, stream>>>(a);
+    }
+    MNB_LAUNCH_CHECK();
+}
+
+template <int Rb>
+void launch_rb(const FftPassArgs& a, cudaStream_t stream) {
+    switch (a.E) {
+        case 2: launch_typed<Rb, 2>(a, stream); break;
+        case 3: launch_typed<Rb, 3>(a, stream); break;
+        case 4: launch_typed<Rb, 4>(a, stream); break;
+        case 6: launch_typed<Rb, 6>(a, stream); break;
+        case 8: launch_typed<Rb, 8>(a, stream); break;
+        case 12: launch_typed<Rb, 12>(a, stream); break;
+        case 16: launch_typed<Rb, 16>(a, stream); break;
+        case 24: launch_typed<Rb, 24>(a, stream); break;
+        default: throw Error(MNB_ERR_INTERNAL, "fft: unsupported elements-per-thread");
+    }
+}
+
+}  // namespace
+
+bool plan_radices(int N, int& E, int* radix, int& nradix) {
+    int m = N, p2 = 0, p3 = 0;
+    while (m % 2 == 0) { m /= 2; ++p2; }
+    while (m % 3 == 0) { m /= 3; ++p3; }
+    if (m != 1) return false;
+    nradix = 0;
+    if (N == 1) { E = 1; return true; }
+    if (p3 == 0) E = N >= 16 ? 16 : N;
+    else if (p2 >= 3) E = 24;
+    else if (p2 == 2) E = 12;
+    else if (p2 == 1) E = 6;
+    else E = 3;
+    int rem = N;
+    const int cand[5] = {16, 8, 4, 3, 2};
+    while (rem > 1) {
+        int pick = 0;
+        for (int R : cand)
+            if (E % R == 0 && rem % R == 0) { pick = R; break; }
+        if (!pick || nradix >= 10) return false;
+        radix[nradix++] = pick;
+        rem /= pick;
+    }
+    return true;
+}
+
+void launch_fft_pass(const FftPassArgs& a, cudaStream_t stream) {
+    if (a.rows <= 0 || a.batches <= 0) return;
+    if (a.N == 1) {
+        dim3 grid(ceil_div(a.rows, 128), unsigned(a.batches));
+        if (a.inverse) fft_len1_kernel<true><<<grid, 128, 0, stream>>>(a);
+        else fft_len1_kernel<false><<<grid, 128, 0, stream>>>(a);
+        MNB_LAUNCH_CHECK();
+        return;
+    }
+    switch (a.Rb) {
+        case 1: launch_rb<1>(a, stream); break;
+        case 4: launch_rb<4>(a, stream); break;
+        case 8: launch_rb<8>(a, stream); break;
+        default: throw Error(MNB_ERR_INTERNAL, "fft: unsupported rows per CTA");
+    }
+}
+
+void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream) {
+    if (a.rows <= 0) return;
+    require(a.rows <= 65535, MNB_ERR_UNSUPPORTED, "direct DFT: too many rows");
+    dim3 grid(ceil_div(a.N, 128), unsigned(a.batches), unsigned(a.rows));
+    if (a.inverse) dft_direct_kernel<true><<<grid, 128, 0, stream>>>(a);
+    else dft_direct_kernel<false><<<grid, 128, 0, stream>>>(a);
+    MNB_LAUNCH_CHECK();
+}
+
+}  // namespace mnb

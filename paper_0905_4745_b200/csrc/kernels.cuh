@@ -1,0 +1,71 @@
+// Launch interfaces of the sm_100a kernels (host-callable).
+#pragma once
+
+#include "common.cuh"
+
+namespace mnb {
+
+// ---------------------------------------------------------------- H stage
+struct HStageArgs {
+    // input element (r, k) = in[in_row0 + r + k*ld_in] (complex, or real promoted)
+    const void* in = nullptr;
+    int in_real = 0, in_conj = 0;
+    int64_t ld_in = 0, in_row0 = 0;
+    const int32_t* gather = nullptr;   // post-gather index i reads column gather[i]
+    const double2* in_diag = nullptr;  // x <- x * diag[src]   (conj if in_diag_conj)
+    int in_diag_conj = 0;
+    const double2* cssn = nullptr;     // (cos theta_j, sin theta_j)
+    const int32_t* halo = nullptr;     // per-chunk start index of the recurrence
+    int adjoint = 0;
+    double2* out = nullptr;
+    int64_t ld_out = 0, out_row0 = 0;
+    const int32_t* scatter = nullptr;  // output index o goes to column scatter[o]
+    const double2* out_diag = nullptr; // y <- y * diag[dst]   (conj if out_diag_conj)
+    int out_diag_conj = 0;
+    int64_t rows = 0, n = 0, chunk = 0, nchunks = 0;
+    int* nonfinite = nullptr;          // if set: flag any non-finite input entry (ProblemInstance::validate)
+};
+void launch_hstage(const HStageArgs& a, cudaStream_t stream);
+
+// ---------------------------------------------------------------- FFT
+enum FftOutMode { FFT_OUT_TWIDDLE = 0, FFT_OUT_SELECT = 1, FFT_OUT_NATURAL = 2 };
+
+struct FftPassArgs {
+    const double2* in = nullptr;
+    int64_t ld_in = 0, in_row0 = 0;
+    int64_t in_bstride = 0, in_istride = 1;  // column = b*in_bstride + idx*in_istride
+    double2* out = nullptr;
+    int64_t ld_out = 0, out_row0 = 0;
+    int mode = FFT_OUT_NATURAL;
+    int64_t out_fstride = 0, out_bstride = 0; // TWIDDLE: column = f*out_fstride + b*out_bstride
+    int64_t nb = 1;                           // SELECT/NATURAL: frequency = b + nb*f
+    const int32_t* sel = nullptr;             // SELECT: frequency -> output slot (or -1)
+    double scale = 1.0;
+    const double2* tw = nullptr;              // w_N^q, q < N   (forward sign)
+    const double2* tw4_hi = nullptr;          // four-step twiddle w_n^e = hi[e>>sh] * lo[e & mask]
+    const double2* tw4_lo = nullptr;
+    int tw4_shift = 0;
+    int64_t n_total = 1;
+    int N = 1;
+    int nradix = 0;
+    int radix[10] = {0};
+    int E = 1;                                // elements per thread
+    int Rb = 1;                               // rows per CTA
+    int64_t rows = 0;                         // rows in this block (masking)
+    int64_t batches = 1;                      // grid.y
+    int inverse = 0;
+};
+void launch_fft_pass(const FftPassArgs& a, cudaStream_t stream);
+// O(N^2) fallback for lengths without a 2^a 3^b factorisation (N <= 4096).
+void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream);
+// Largest per-thread element count E (and radix plan) for an in-smem length N;
+// returns false when N has prime factors other than 2 and 3.
+bool plan_radices(int N, int& E, int* radix, int& nradix);
+
+// ---------------------------------------------------------------- misc
+void launch_copy_dups(double2* S, int64_t ldS, int64_t row0, int64_t rows, const int32_t* dups, int64_t ndups,
+                      cudaStream_t stream);
+void launch_scatter_add_sample(const double2* v, int64_t l, const int32_t* sample, int with_replacement,
+                               double2* w, int64_t n, cudaStream_t stream);
+
+}  // namespace mnb

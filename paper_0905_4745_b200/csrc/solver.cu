@@ -1,0 +1,539 @@
+// The randomized minimal-norm solve on the GPU (src/solver.cpp:50-128) and
+// its least-squares subsolver (src/lsq.cpp:43-113).
+//
+//   Step 1  S = T·A^H                     sketch_matrix  (SRFT kernels)
+//   Step 2  S = QR, z = Q [R^{-H} b; 0]    cuSOLVER geqrf / cuBLAS trsv / unmqr
+//   Step 3  c = T^* z                      srft_adjoint_vec
+//   Step 4  E = T'·A^H, E = Q'R', CG on the normal equations of A^H R'^{-1}
+//           (fused pass kernel, explicit R'^{-1} from trtri, device-side loop)
+//   Step 5  x = A^H y, ||A x - b||         one more fused pass
+//
+// Multi-GPU (column-sharded A): one NCCL allreduce of [s, qq, <r,t>, ||r||^2]
+// (2m+4 doubles) per CG iteration; the sketch redistributes A with one
+// all-to-all (srft_gpu.cu).  The small m-space work is replicated per rank.
+#include <chrono>
+#include <cmath>
+#include <future>
+#include <thread>
+
+#include "context.cuh"
+
+namespace mnb {
+
+namespace {
+
+constexpr double kEps = 2.220446049250313080847e-16;
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void cusolver_check(cusolverStatus_t s, const char* what) {
+    if (s != CUSOLVER_STATUS_SUCCESS) throw Error(MNB_ERR_CUDA, std::string(what) + " failed (cusolver status " + std::to_string(int(s)) + ")");
+}
+void cublas_check(cublasStatus_t s, const char* what) {
+    if (s != CUBLAS_STATUS_SUCCESS) throw Error(MNB_ERR_CUDA, std::string(what) + " failed (cublas status " + std::to_string(int(s)) + ")");
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(MNB_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+template <class T>
+T* dev(DevBuf& b, size_t count) {
+    return static_cast<T*>(b.ensure(count * sizeof(T) + 16));
+}
+
+// Householder QR of the tall l x m sketch in place (Eigen::HouseholderQR at
+// src/solver.cpp:86 and src/lsq.cpp:58; LAPACK/cuSOLVER use the same
+// reflector convention R_jj = -sign(Re x0)||x||).
+void qr_in_place(Context& ctx, double2* S, int64_t l, int64_t m, double2* tau) {
+    size_t dws = 0, hws = 0;
+    cusolver_check(cusolverDnXgeqrf_bufferSize(ctx.cusolver, ctx.cusolver_params, l, m, CUDA_C_64F, S, l, CUDA_C_64F,
+                                               tau, CUDA_C_64F, &dws, &hws),
+                   "geqrf_bufferSize");
+    void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+    if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+    int* info = dev<int>(ctx.qr_info, 1);
+    cusolver_check(cusolverDnXgeqrf(ctx.cusolver, ctx.cusolver_params, l, m, CUDA_C_64F, S, l, CUDA_C_64F, tau,
+                                    CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
+                   "geqrf");
+}
+
+// src/lsq.cpp:18-27 / src/solver.cpp:25-33: entries |R_jj| < rows*eps*max|R_jj| (or exactly 0).
+int64_t deficient_count(Context& ctx, const double2* QR, int64_t ld, int64_t m, int64_t rows) {
+    std::vector<double> diag(size_t(2 * m));
+    MNB_CUDA(cudaMemcpy2DAsync(diag.data(), 16, QR, size_t(ld + 1) * 16, 16, size_t(m), cudaMemcpyDeviceToHost,
+                               ctx.stream));
+    MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    double dmax = 0.0;
+    for (int64_t j = 0; j < m; ++j) dmax = std::max(dmax, std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]));
+    const double thr = double(rows) * kEps * dmax;
+    int64_t bad = 0;
+    for (int64_t j = 0; j < m; ++j) {
+        const double re = diag[size_t(2 * j)], im = diag[size_t(2 * j + 1)];
+        if (std::hypot(re, im) < thr || (re == 0.0 && im == 0.0)) ++bad;
+    }
+    return bad;
+}
+
+void allreduce_sum(Context& ctx, double* buf, size_t count) {
+    if (ctx.world > 1) nccl_check(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm, ctx.stream), "ncclAllReduce");
+}
+
+struct PassBuffers {
+    PcgPlan plan;
+    double2 *part_s;
+    double *part_scal, *red;
+};
+
+PassBuffers pass_buffers(Context& ctx) {
+    PassBuffers b;
+    b.plan = plan_pcg_pass(ctx.m, std::max<int64_t>(ctx.n_local, 1), ctx.dtype == MNB_F64, ctx.num_sms);
+    b.part_s = dev<double2>(ctx.part_s, size_t(b.plan.grid) * size_t(ctx.m));
+    b.part_scal = dev<double>(ctx.part_scal, size_t(b.plan.grid) * 4);
+    b.red = dev<double>(ctx.red, size_t(2 * ctx.m + 4));
+    return b;
+}
+
+// One fused pass + deterministic reduction (+ allreduce across ranks).
+void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w, const double2* tin, double2* tout,
+                double2* r, const CgState* state) {
+    if (ctx.n_local > 0) {
+        PcgPassArgs a;
+        a.A = ctx.A;
+        a.is_real = ctx.dtype == MNB_F64;
+        a.m = ctx.m;
+        a.n = ctx.n_local;
+        a.w = w;
+        a.tin = tin;
+        a.tout = tout;
+        a.r = r;
+        a.state = state;
+        a.part_s = pb.part_s;
+        a.part_scal = pb.part_scal;
+        a.mode = mode;
+        launch_pcg_pass(a, pb.plan, ctx.stream);
+        launch_pcg_reduce(pb.part_s, pb.part_scal, pb.plan.grid, ctx.m, pb.red, state, ctx.stream);
+        ctx.launches += 2;
+    } else {
+        MNB_CUDA(cudaMemsetAsync(pb.red, 0, size_t(2 * ctx.m + 4) * 8, ctx.stream));
+    }
+    allreduce_sum(ctx, pb.red, size_t(2 * ctx.m + 4));
+}
+
+}  // namespace
+
+void sync(Context& ctx) { MNB_CUDA(cudaStreamSynchronize(ctx.stream)); }
+
+Context::~Context() {
+    for (auto e : events) if (e) cudaEventDestroy(e);
+    if (cusolver_params) cusolverDnDestroyParams(cusolver_params);
+    if (cusolver) cusolverDnDestroy(cusolver);
+    if (cublas) cublasDestroy(cublas);
+    if (comm) ncclCommDestroy(comm);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+cudaEvent_t Context::event(size_t i) {
+    while (events.size() <= i) {
+        cudaEvent_t e;
+        MNB_CUDA(cudaEventCreate(&e));
+        events.push_back(e);
+    }
+    return events[i];
+}
+
+// ------------------------------------------------------------- CG loop ----
+// solve_least_squares (src/lsq.cpp:43-113) from the sketch R' onward.
+// c: this rank's n_local entries (device).  y: m entries (device).
+LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
+                 double dup, double2* y, bool want_norms) {
+    const int64_t m = ctx.m, n = ctx.n_local;
+    LsqResult res;
+    const double t0 = now_s();
+    // explicit R'^{-1} (consistent forward/adjoint preconditioner)
+    double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
+    double2* Rinv_rows = dev<double2>(ctx.Rinv_rows, size_t(m) * size_t(m));
+    MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, Rtop, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
+                               cudaMemcpyDeviceToDevice, ctx.stream));
+    {
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
+                                                   CUDA_C_64F, Rinv, m, &dws, &hws),
+                       "trtri_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXtrtri(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m, CUDA_C_64F, Rinv,
+                                        m, work, dws, ctx.host_work.data(), hws, dev<int>(ctx.qr_info, 1)),
+                       "trtri");
+    }
+    launch_transpose(Rinv, m, m, m, Rinv_rows, m, ctx.stream);
+    ctx.launches += 1;
+
+    double2* w = dev<double2>(ctx.vec_m[0], size_t(m));
+    double2* u = dev<double2>(ctx.vec_m[1], size_t(m));
+    double2* g = dev<double2>(ctx.vec_m[2], size_t(m));
+    double2* dir = dev<double2>(ctx.vec_m[3], size_t(m));
+    double2* dir_old = dev<double2>(ctx.vec_m[4], size_t(m));
+    double2* r = dev<double2>(ctx.vec_n[0], size_t(std::max<int64_t>(n, 1)));
+    double2* t = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(n, 1)));
+    CgState* st = dev<CgState>(ctx.state, 1);
+    double* norms = dev<double>(ctx.resid, size_t(max_it + 2));
+    const int ub = pcg_upd_blocks(m);
+    double* part_gg = dev<double>(ctx.part_gg, size_t(ub));
+    PassBuffers pb = pass_buffers(ctx);
+
+    launch_init_state(st, tau, dup, (long long)max_it, ctx.stream);
+    // initial state (lsq.cpp:77-86): r = c, g = M^H c, dir = g
+    cudaEvent_t ea = ctx.event(20), eb = ctx.event(21);
+    MNB_CUDA(cudaEventRecord(ea, ctx.stream));
+    fused_pass(ctx, pb, PCG_INIT, nullptr, c, t, r, nullptr);
+    MNB_CUDA(cudaEventRecord(eb, ctx.stream));
+    launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 1, ctx.stream);
+    launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 1, ctx.stream);
+    ctx.launches += 3;
+
+    int* done_h = static_cast<int*>(ctx.pin_small.ensure(sizeof(CgState) + 64));
+    CgState* st_h = reinterpret_cast<CgState*>(done_h);
+    auto read_state = [&]() {
+        MNB_CUDA(cudaMemcpyAsync(st_h, st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    };
+    // CG iterations (lsq.cpp:88-107), K at a time between host polls of the
+    // device-side done flag; kernels of finished loops exit immediately.
+    const int64_t K = 4;
+    int64_t issued = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pass_ev;
+    for (;;) {
+        read_state();
+        if (st_h->done || issued >= max_it + 1) break;
+        for (int64_t k = 0; k < K; ++k) {
+            cudaEvent_t e0 = ctx.event(32 + 2 * size_t(issued)), e1 = ctx.event(33 + 2 * size_t(issued));
+            MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+            fused_pass(ctx, pb, PCG_CG, w, t, t, r, st);
+            MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+            pass_ev.emplace_back(e0, e1);
+            launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 0, ctx.stream);
+            launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 0, ctx.stream);
+            ctx.launches += 2;
+            ++issued;
+        }
+    }
+    // exact final residual and y = R'^{-1} u (lsq.cpp:109-111)
+    double* scratch = dev<double>(ctx.scratch, 512);
+    if (n > 0) {
+        launch_pcg_finalize(r, t, n, st, scratch, ctx.stream);
+        ctx.launches += 2;
+    } else {
+        MNB_CUDA(cudaMemsetAsync(&st->rr_final, 0, 8, ctx.stream));
+    }
+    allreduce_sum(ctx, &st->rr_final, 1);
+    launch_trmv_rows(Rinv_rows, m, u, y, ctx.stream);
+    ctx.launches += 1;
+    read_state();
+    res.iterations = st_h->iterations;
+    res.converged = st_h->converged != 0;
+    res.rr0 = st_h->rr0;
+    const double rr = st_h->rr_final, excess = st_h->excess;
+    const double min_est = std::max(rr - excess, 0.0);
+    res.achieved_excess = min_est > 0.0 ? excess / min_est : 0.0;
+    // device time of the passes that did work: the INIT pass + one per iteration
+    float ms = 0.f;
+    MNB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
+    res.pass_ms = ms;
+    res.pass_launches = 1;
+    const int64_t worked = std::min<int64_t>(int64_t(pass_ev.size()), res.iterations + (st_h->stop_qq0 ? 1 : 0));
+    for (int64_t i = 0; i < worked; ++i) {
+        MNB_CUDA(cudaEventElapsedTime(&ms, pass_ev[size_t(i)].first, pass_ev[size_t(i)].second));
+        res.pass_ms += ms;
+        res.pass_launches += 1;
+    }
+    if (want_norms) {
+        res.residual_norms.resize(size_t(res.iterations + 1));
+        MNB_CUDA(cudaMemcpy(res.residual_norms.data(), norms, size_t(res.iterations + 1) * 8, cudaMemcpyDeviceToHost));
+        res.residual_norms[size_t(res.iterations)] = std::sqrt(rr);
+    }
+    res.pcg_seconds = now_s() - t0;
+    return res;
+}
+
+// ------------------------------------------------------------- helpers ----
+struct SketchQr {
+    double2* S;
+    double2* tau;
+};
+
+SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, double* kernel_ms,
+                       double* sketch_s, double* qr_s, double* redistribute_s) {
+    const int64_t l = op.host->l, m = ctx.m;
+    double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
+    double2* tau = dev<double2>(taubuf, size_t(m));
+    cudaEvent_t e0 = ctx.event(12), e1 = ctx.event(13), e2 = ctx.event(14);
+    MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+    sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
+    MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+    qr_in_place(ctx, S, l, m, tau);
+    MNB_CUDA(cudaEventRecord(e2, ctx.stream));
+    MNB_CUDA(cudaEventSynchronize(e2));
+    float a = 0.f, b = 0.f;
+    MNB_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    MNB_CUDA(cudaEventElapsedTime(&b, e1, e2));
+    if (sketch_s) *sketch_s += a * 1e-3;
+    if (qr_s) *qr_s += b * 1e-3;
+    return {S, tau};
+}
+
+unsigned char* pinned_alloc(PinnedBuf& pb, size_t bytes) { return static_cast<unsigned char*>(pb.ensure(bytes)); }
+
+void validate_matrix_set(const Context& ctx) {
+    require(ctx.A != nullptr || ctx.n_local == 0, MNB_ERR_INVALID_ARGUMENT, "no problem matrix set (mnb_set_matrix)");
+}
+
+// ---------------------------------------------------- solve_randomized ----
+void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
+                      double2* c_dev, mnb_solve_report& rep) {
+    const double t_start = now_s();
+    validate_matrix_set(ctx);
+    const int64_t m = ctx.m, n = ctx.n_global;
+    // ProblemInstance::validate (src/solver.cpp:37-48); A's finiteness is checked on the device below.
+    if (m < 1 || m >= n)
+        throw Error(MNB_ERR_DIMENSION, "problem must be underdetermined: 1 <= m < n, got m=" + std::to_string(m) +
+                                           ", n=" + std::to_string(n));
+    bool b_finite = true, b_zero = true;
+    for (int64_t i = 0; i < 2 * m; ++i) {
+        const double v = reinterpret_cast<const double*>(b_host)[i];
+        b_finite = b_finite && std::isfinite(v);
+        b_zero = b_zero && v == 0.0;
+    }
+    if (!b_finite) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
+    if (!(cfg.epsilon > 0.0 && cfg.epsilon < 1.0)) throw Error(MNB_ERR_CONFIG, "epsilon must lie in (0, 1)");
+    if (!(cfg.alpha > 1.0)) throw Error(MNB_ERR_CONFIG, "alpha must exceed 1");
+    const int64_t l = cfg.sketch_size > 0 ? cfg.sketch_size : 4 * m;
+    if (l <= m || l >= n)
+        throw Error(MNB_ERR_CONFIG, "sketch size l=" + std::to_string(l) + " must satisfy m < l < n (m=" +
+                                        std::to_string(m) + ", n=" + std::to_string(n) +
+                                        "); this system is outside the randomized solver's regime - use the "
+                                        "classical solver instead");
+    rep = mnb_solve_report{};
+    rep.sketch_size = l;
+    rep.lsq_tau = cfg.epsilon * cfg.epsilon * double(l) / (cfg.alpha * double(n));
+    rep.world_size = ctx.world;
+    rep.lsq_converged = 1;
+    const int64_t launches0 = ctx.launches;
+    if (b_zero) {  // src/solver.cpp:68-73
+        if (ctx.n_local) {
+            MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(ctx.n_local) * 16, ctx.stream));
+            if (c_dev) MNB_CUDA(cudaMemsetAsync(c_dev, 0, size_t(ctx.n_local) * 16, ctx.stream));
+        }
+        sync(ctx);
+        rep.total_seconds = now_s() - t_start;
+        return;
+    }
+    const int sampling = cfg.sampling;
+    const RandomStream root(cfg.seed);
+    const uint64_t seed_T = root.derive_seed(11), seed_Tp = root.derive_seed(12);  // src/solver.cpp:19
+    const int hw = int(std::max(2u, std::thread::hardware_concurrency()));
+    // Both operators are drawn concurrently on the host; T' overlaps Steps 1-3 on the GPU.
+    SrftHost T, Tp;
+    auto noop = [](unsigned char*) {};
+    const double tp0 = now_s();
+    double t_param_T = 0.0, t_param_Tp = 0.0;
+    auto fut_Tp = std::async(std::launch::async, [&] {
+        const double s = now_s();
+        build_srft_host(Tp, l, n, seed_Tp, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); },
+                        noop, hw / 2);
+        t_param_Tp = now_s() - s;
+    });
+    try {
+        build_srft_host(T, l, n, seed_T, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); },
+                        noop, hw - hw / 2);
+    } catch (...) {
+        fut_Tp.wait();
+        throw;
+    }
+    t_param_T = now_s() - tp0;
+
+    // ---- Step 1: S = T A^*
+    double t0 = now_s();
+    SrftDev Td;
+    upload_srft(ctx, T, Td);
+    int* nonfinite = dev<int>(ctx.flag, 1);
+    MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx.stream));
+    ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
+    double qr_s = 0.0, sk_s = 0.0;
+    SketchQr sq = sketch_and_qr(ctx, Td, ctx.sk_S, ctx.tau_S, rep.sketch_kernel_ms, &sk_s, &qr_s,
+                                &rep.redistribute_seconds);
+    ctx.nonfinite = nullptr;
+    {
+        int flag = 0;
+        MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        sync(ctx);
+        if (ctx.world > 1) {
+            int* f = dev<int>(ctx.flag, 1);
+            nccl_check(ncclAllReduce(f, f, 1, ncclInt, ncclMax, ctx.comm, ctx.stream), "ncclAllReduce");
+            MNB_CUDA(cudaMemcpyAsync(&flag, f, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+            sync(ctx);
+        }
+        if (flag) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
+    }
+    rep.sketch_seconds[0] = sk_s;
+    rep.qr_seconds[0] = qr_s;
+    rep.step_seconds[0] = now_s() - t0;
+
+    // ---- Step 2: z = Q [R^{-H} b; 0]  (src/solver.cpp:85-97)
+    t0 = now_s();
+    if (int64_t bad = deficient_count(ctx, sq.S, l, m, l); bad > 0)
+        throw Error(MNB_ERR_RANK_DEFICIENCY,
+                    "sketch S = T A* lost rank (" + std::to_string(bad) +
+                        " dependent columns); the problem matrix is rank deficient",
+                    bad);
+    double2* z = dev<double2>(ctx.rhs, size_t(l));
+    MNB_CUDA(cudaMemsetAsync(z, 0, size_t(l) * 16, ctx.stream));
+    MNB_CUDA(cudaMemcpyAsync(z, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
+                             reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l), reinterpret_cast<cuDoubleComplex*>(z), 1),
+                 "ztrsv");
+    {
+        int lwork = 0;
+        cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
+                                                   reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
+                                                   reinterpret_cast<const cuDoubleComplex*>(sq.tau),
+                                                   reinterpret_cast<const cuDoubleComplex*>(z), int(l), &lwork),
+                       "unmqr_bufferSize");
+        auto* work = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
+        cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
+                                        reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
+                                        reinterpret_cast<const cuDoubleComplex*>(sq.tau),
+                                        reinterpret_cast<cuDoubleComplex*>(z), int(l), work, lwork,
+                                        dev<int>(ctx.qr_info, 1)),
+                       "unmqr");
+    }
+    sync(ctx);
+    rep.step_seconds[1] = now_s() - t0;
+
+    // ---- Step 3: c = T^* z  (src/solver.cpp:100-102)
+    t0 = now_s();
+    double2* c_vec = dev<double2>(ctx.vec_n[2], size_t(n));
+    srft_adjoint_vec(ctx, Td, z, c_vec);
+    const double2* c_loc = c_vec + ctx.col_begin;
+    sync(ctx);
+    rep.step_seconds[2] = now_s() - t0;
+
+    // ---- Step 4: y = argmin ||A^* y - c||  (src/solver.cpp:104-114, src/lsq.cpp:43-113)
+    t0 = now_s();
+    fut_Tp.get();
+    rep.param_seconds = t_param_T + t_param_Tp;
+    SrftDev Tpd;
+    upload_srft(ctx, Tp, Tpd);
+    sk_s = 0.0;
+    qr_s = 0.0;
+    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, rep.sketch_kernel_ms, &sk_s, &qr_s,
+                                &rep.redistribute_seconds);
+    rep.sketch_seconds[1] = sk_s;
+    rep.qr_seconds[1] = qr_s;
+    if (int64_t bad = deficient_count(ctx, eq.S, l, m, n); bad > 0)
+        throw Error(MNB_ERR_RANK_DEFICIENCY,
+                    "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
+                    bad);
+    double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
+    LsqResult ls = run_cg(ctx, c_loc, eq.S, l, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false);
+    rep.lsq_iterations = ls.iterations;
+    rep.lsq_converged = ls.converged ? 1 : 0;
+    rep.lsq_achieved_excess = ls.achieved_excess;
+    rep.pcg_seconds = ls.pcg_seconds;
+    rep.pcg_pass_ms_sum = ls.pass_ms;
+    rep.pcg_pass_launches = ls.pass_launches;
+    rep.step_seconds[3] = now_s() - t0;
+
+    // ---- Step 5: x = A^* y, residual ||A x - b|| (src/solver.cpp:118-125)
+    t0 = now_s();
+    PassBuffers pb = pass_buffers(ctx);
+    fused_pass(ctx, pb, PCG_APPLY, y, nullptr, x_dev, nullptr, nullptr);
+    std::vector<double> red(size_t(2 * m + 4));
+    MNB_CUDA(cudaMemcpyAsync(red.data(), pb.red, red.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    if (c_dev && ctx.n_local)
+        MNB_CUDA(cudaMemcpyAsync(c_dev, c_loc, size_t(ctx.n_local) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    sync(ctx);
+    rep.step_seconds[4] = now_s() - t0;
+    double res2 = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+        const double dr = red[size_t(2 * i)] - reinterpret_cast<const double*>(b_host)[2 * i];
+        const double di = red[size_t(2 * i + 1)] - reinterpret_cast<const double*>(b_host)[2 * i + 1];
+        res2 += dr * dr + di * di;
+    }
+    rep.residual_norm = std::sqrt(res2);
+    const double xnorm = std::sqrt(red[size_t(2 * m)]);
+    rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
+    rep.kernel_launches = ctx.launches - launches0;
+    rep.total_seconds = now_s() - t_start;
+}
+
+// ------------------------------------------------ solve_least_squares -----
+void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
+                         double* residual_norms, mnb_lsq_solution& sol) {
+    validate_matrix_set(ctx);
+    const int64_t m = ctx.m, n = ctx.n_global;  // B = A^H is n x m
+    // src/lsq.cpp:45-53
+    if (m < 1 || n <= m) throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: B must be tall (n > m >= 1)");
+    if (cfg.sketch_size <= m || cfg.sketch_size > n)
+        throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: sketch size must lie in (m, n]");
+    if (!(cfg.tau > 0.0)) throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: tau must be positive");
+    if (cfg.max_iterations < 1)
+        throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: max_iterations must be at least 1");
+    SrftHost Tp;
+    build_srft_host(Tp, cfg.sketch_size, n, cfg.stream_seed, cfg.sampling,
+                    [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); }, [](unsigned char*) {}, 0);
+    SrftDev Tpd;
+    upload_srft(ctx, Tp, Tpd);
+    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, nullptr, nullptr, nullptr, nullptr);
+    if (int64_t bad = deficient_count(ctx, eq.S, cfg.sketch_size, m, n); bad > 0)
+        throw Error(MNB_ERR_RANK_DEFICIENCY,
+                    "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
+                    bad);
+    double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
+    LsqResult ls = run_cg(ctx, c_dev, eq.S, cfg.sketch_size, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
+                          residual_norms != nullptr);
+    MNB_CUDA(cudaMemcpyAsync(y_host, y, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
+    sync(ctx);
+    sol.achieved_excess = ls.achieved_excess;
+    sol.iterations = ls.iterations;
+    sol.converged = ls.converged ? 1 : 0;
+    if (residual_norms)
+        for (size_t i = 0; i < ls.residual_norms.size(); ++i) residual_norms[i] = ls.residual_norms[i];
+}
+
+// ----------------------------------------------------------- benchmark ----
+double bench_pcg_pass(Context& ctx, int reps) {
+    validate_matrix_set(ctx);
+    const int64_t m = ctx.m;
+    PassBuffers pb = pass_buffers(ctx);
+    double2* w = dev<double2>(ctx.vec_m[0], size_t(m));
+    std::vector<double> wh(size_t(2 * m));
+    for (int64_t i = 0; i < 2 * m; ++i) wh[size_t(i)] = 1.0 / double(1 + i % 7);
+    MNB_CUDA(cudaMemcpyAsync(w, wh.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    double2* t = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(ctx.n_local, 1)));
+    fused_pass(ctx, pb, PCG_APPLY, w, nullptr, t, nullptr, nullptr);  // warm-up
+    cudaEvent_t e0 = ctx.event(40), e1 = ctx.event(41);
+    MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+    for (int i = 0; i < reps; ++i) {
+        PcgPassArgs a;
+        a.A = ctx.A;
+        a.is_real = ctx.dtype == MNB_F64;
+        a.m = m;
+        a.n = ctx.n_local;
+        a.w = w;
+        a.tout = t;
+        a.part_s = pb.part_s;
+        a.part_scal = pb.part_scal;
+        a.mode = PCG_APPLY;
+        launch_pcg_pass(a, pb.plan, ctx.stream);
+        ctx.launches += 1;
+    }
+    MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+    MNB_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    return double(ms) / reps;
+}
+
+}  // namespace mnb

@@ -1,0 +1,460 @@
+// The SRFT on the GPU: sketch T·A^H (SrftOperator::apply_to_columns,
+// src/srft.cpp:147-153), single-vector apply / apply_adjoint
+// (src/srft.cpp:115-145) and the unitary DFT (src/fft.cpp:90-110).
+//
+// Sketch data flow for a slab of rows (all column-major, one column = the
+// slab's rows contiguous):
+//   P1  hstage: x1[:, i] = zeta[i] * Chain~( zeta~[p~[i]] * conj(A[:, p~[i]]) )   (H right half)
+//   P2  hstage: x2[:, i] = d[i]    * Chain ( x1[:, p[i]] )                        (H left half, D)
+//   FA  fft:    length-n2 DFTs over k2 of x2[:, k1 + n1 k2], twiddle w_n^{f2 k1} -> x1[:, f2 n1 + k1]
+//   FB  fft:    length-n1 DFTs over k1, keep sampled f = f2 + n2 f1, scale n^{-1/2} -> S
+// (n <= 2048: one FFT launch does the whole transform and the sampling.)
+#include <cmath>
+
+#include "context.cuh"
+
+namespace mnb {
+
+namespace {
+
+void fill_twiddles(DevBuf& buf, int64_t N, int64_t count, int64_t step, cudaStream_t stream) {
+    // buf[q] = exp(-2 pi i (q*step mod N) / N), computed in long double, rounded once.
+    std::vector<double> h(size_t(2 * count));
+    const long double two_pi = 6.283185307179586476925286766559L;
+    for (int64_t q = 0; q < count; ++q) {
+        const int64_t e = (q * step) % N;
+        const long double ang = two_pi * (long double)e / (long double)N;
+        h[size_t(2 * q)] = double(cosl(ang));
+        h[size_t(2 * q + 1)] = double(-sinl(ang));
+    }
+    buf.ensure(size_t(count) * 16);
+    MNB_CUDA(cudaMemcpyAsync(buf.p, h.data(), size_t(count) * 16, cudaMemcpyHostToDevice, stream));
+    MNB_CUDA(cudaStreamSynchronize(stream));
+}
+
+bool smooth(int64_t N) {
+    int E, r[10], nr;
+    return N <= 1 || (N <= 8192 && plan_radices(int(N), E, r, nr));
+}
+
+void make_len_plan(FftLenPlan& p, int64_t N, cudaStream_t stream) {
+    p.N = int(N);
+    p.direct = !plan_radices(int(N), p.E, p.radix, p.nradix);
+    fill_twiddles(p.tw, N, N, 1, stream);
+}
+
+int rows_per_cta(int N) { return N <= 1024 ? 8 : 4; }
+
+FftPassArgs base_args(const FftLenPlan& p) {
+    FftPassArgs a;
+    a.N = p.N;
+    a.E = p.E;
+    a.nradix = p.nradix;
+    for (int i = 0; i < p.nradix; ++i) a.radix[i] = p.radix[i];
+    a.tw = p.tw.as<double2>();
+    return a;
+}
+
+void run_fft(Context& ctx, const FftLenPlan& p, FftPassArgs a) {
+    if (p.direct) launch_dft_direct(a, ctx.stream);
+    else launch_fft_pass(a, ctx.stream);
+    ctx.launches += 1;
+}
+
+struct EventTimer {
+    Context& ctx;
+    double* acc;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    EventTimer(Context& c, double* a, size_t slot) : ctx(c), acc(a) {
+        if (acc) {
+            e0 = ctx.event(2 * slot);
+            e1 = ctx.event(2 * slot + 1);
+            MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+        }
+    }
+    void stop() {
+        if (acc) {
+            MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+            MNB_CUDA(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            *acc += ms;
+        }
+    }
+};
+
+
+// Length-n DFT of `rows` rows: in (col-major, ld_in) -> out.  SELECT keeps the
+// sampled frequencies (out[slot + (out_row0 + r) * ld_out]); NATURAL writes
+// all of them (out[(out_row0 + r) + f * ld_out]).  Scaled by n^{-1/2}.
+void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t rows, double2* tmp, int64_t ld_tmp,
+              double2* out, int64_t ld_out, int64_t out_row0, bool select, const int32_t* sel, bool inverse,
+              double* ms_a, double* ms_b) {
+    FftPlan& P = ctx.fft_plan(n);
+    const double scale = 1.0 / std::sqrt(double(n));
+    auto rb = [&](int N) { return rows == 1 ? 1 : rows_per_cta(N); };
+    if (P.single) {
+        FftPassArgs a = base_args(P.A);
+        a.in = in;
+        a.ld_in = ld_in;
+        a.in_bstride = 0;
+        a.in_istride = 1;
+        a.out = out;
+        a.ld_out = ld_out;
+        a.out_row0 = out_row0;
+        a.mode = select ? FFT_OUT_SELECT : FFT_OUT_NATURAL;
+        a.nb = 1;
+        a.sel = sel;
+        a.scale = scale;
+        a.Rb = rb(P.A.N);
+        a.rows = rows;
+        a.batches = 1;
+        a.inverse = inverse;
+        EventTimer t(ctx, ms_a, 2);
+        run_fft(ctx, P.A, a);
+        t.stop();
+        return;
+    }
+    {
+        FftPassArgs a = base_args(P.A);
+        a.in = in;
+        a.ld_in = ld_in;
+        a.in_bstride = 1;
+        a.in_istride = P.n1;
+        a.out = tmp;
+        a.ld_out = ld_tmp;
+        a.mode = FFT_OUT_TWIDDLE;
+        a.out_fstride = P.n1;
+        a.out_bstride = 1;
+        a.tw4_hi = P.tw4_hi.as<double2>();
+        a.tw4_lo = P.tw4_lo.as<double2>();
+        a.tw4_shift = P.tw4_shift;
+        a.n_total = n;
+        a.Rb = rb(P.A.N);
+        a.rows = rows;
+        a.batches = P.n1;
+        a.inverse = inverse;
+        EventTimer t(ctx, ms_a, 2);
+        run_fft(ctx, P.A, a);
+        t.stop();
+    }
+    {
+        FftPassArgs a = base_args(P.B);
+        a.in = tmp;
+        a.ld_in = ld_tmp;
+        a.in_bstride = P.n1;
+        a.in_istride = 1;
+        a.out = out;
+        a.ld_out = ld_out;
+        a.out_row0 = out_row0;
+        a.mode = select ? FFT_OUT_SELECT : FFT_OUT_NATURAL;
+        a.nb = P.n2;
+        a.sel = sel;
+        a.scale = scale;
+        a.Rb = rb(P.B.N);
+        a.rows = rows;
+        a.batches = P.n2;
+        a.inverse = inverse;
+        EventTimer t(ctx, ms_b, 3);
+        run_fft(ctx, P.B, a);
+        t.stop();
+    }
+}
+}  // namespace
+
+FftPlan& Context::fft_plan(int64_t n) {
+    auto it = fft_plans.find(n);
+    if (it != fft_plans.end()) return *it->second;
+    auto plan = std::make_unique<FftPlan>();
+    FftPlan& P = *plan;
+    P.n = n;
+    if (n <= 2048 || (n <= 4096 && !smooth(n))) {
+        P.single = true;
+        P.n1 = 1;
+        P.n2 = n;
+        make_len_plan(P.A, n, stream);
+    } else {
+        // n = n1 * n2 with both factors smooth and <= 2048, as balanced as possible
+        int64_t best = 0;
+        for (int64_t n2 = 2; n2 <= 2048; ++n2) {
+            if (n % n2) continue;
+            const int64_t n1 = n / n2;
+            if (n1 > 2048 || !smooth(n1) || !smooth(n2)) continue;
+            if (!best || std::llabs(n1 - n2) < std::llabs(n / best - best)) best = n2;
+        }
+        require(best != 0, MNB_ERR_UNSUPPORTED,
+                "FFT length " + std::to_string(n) + " is not supported on the GPU (needs n <= 4096, or n = n1*n2 "
+                "with n1, n2 <= 2048 of the form 2^a 3^b)");
+        P.single = false;
+        P.n2 = best;
+        P.n1 = n / best;
+        make_len_plan(P.A, P.n2, stream);
+        make_len_plan(P.B, P.n1, stream);
+        int shift = 0;
+        while ((int64_t(1) << (2 * shift)) < n) ++shift;
+        P.tw4_shift = shift;
+        const int64_t lo = int64_t(1) << shift, hi = (n + lo - 1) / lo;
+        fill_twiddles(P.tw4_lo, n, lo, 1, stream);
+        fill_twiddles(P.tw4_hi, n, hi, lo, stream);
+    }
+    fft_plans[n] = std::move(plan);
+    return P;
+}
+
+void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
+    dev.host = &op;
+    dev.blob.ensure(op.device_bytes);
+    MNB_CUDA(cudaMemcpyAsync(dev.blob.p, op.blob, op.device_bytes, cudaMemcpyHostToDevice, ctx.stream));
+    dev.ndups = int64_t(op.dups.size() / 2);
+    if (dev.ndups) {
+        dev.dups.ensure(op.dups.size() * 4);
+        MNB_CUDA(cudaMemcpyAsync(dev.dups.p, op.dups.data(), op.dups.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // op.dups is pageable
+    }
+    ctx.fft_plan(op.n);
+}
+
+static HStageArgs chain_args(const SrftDev& op, bool tilde, bool adjoint) {
+    const SrftHost& h = *op.host;
+    HStageArgs a;
+    a.cssn = op.at<double2>(tilde ? h.off_cssn_tilde : h.off_cssn);
+    const int32_t* halo = op.at<int32_t>(h.off_halo);
+    const int64_t nc = h.ch.nchunks;
+    a.halo = halo + (adjoint ? 2 * nc : 0) + (tilde ? nc : 0);
+    a.adjoint = adjoint ? 1 : 0;
+    a.n = h.n;
+    a.chunk = h.ch.chunk;
+    a.nchunks = nc;
+    return a;
+}
+
+void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real, int64_t lda, int64_t row0,
+                  int64_t rows, double2* out, int64_t ldo, int64_t out_row0, double* kernel_ms) {
+    const SrftHost& h = *op.host;
+    const int64_t n = h.n;
+    ctx.fft_plan(n);
+    // slab height: two n-column intermediates per slab row
+    size_t free_b = 0, total_b = 0;
+    MNB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t have = ctx.ws_x1.bytes + ctx.ws_x2.bytes + free_b;
+    const size_t budget = have > (size_t(3) << 30) ? have - (size_t(3) << 30) : have / 2;
+    int64_t Ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
+    if (Ms < rows) Ms = std::max<int64_t>(8, Ms & ~int64_t(7));
+    Ms = std::max<int64_t>(1, std::min<int64_t>(Ms, rows));
+    double2* x1 = static_cast<double2*>(ctx.ws_x1.ensure(size_t(Ms) * size_t(n) * 16));
+    double2* x2 = static_cast<double2*>(ctx.ws_x2.ensure(size_t(Ms) * size_t(n) * 16));
+    const double scale = 1.0 / std::sqrt(double(n));
+
+    for (int64_t s0 = 0; s0 < rows; s0 += Ms) {
+        const int64_t rs = std::min(Ms, rows - s0);
+        {  // P1: Z~, Pi~, Theta~, Z   (src/srft.cpp:52-55)
+            HStageArgs a = chain_args(op, true, false);
+            a.in = Ablk;
+            a.in_real = is_real;
+            a.in_conj = 1;  // column of B = A^H is conj(row of A)
+            a.ld_in = lda;
+            a.in_row0 = row0 + s0;
+            a.nonfinite = ctx.nonfinite;
+            a.gather = op.at<int32_t>(h.off_perm_tilde);
+            a.in_diag = op.at<double2>(h.off_zeta_tilde);
+            a.out = x1;
+            a.ld_out = Ms;
+            a.out_diag = op.at<double2>(h.off_zeta);
+            a.rows = rs;
+            EventTimer t(ctx, kernel_ms ? &kernel_ms[0] : nullptr, 0);
+            launch_hstage(a, ctx.stream);
+            ctx.launches += 1;
+            t.stop();
+        }
+        {  // P2: Pi, Theta, then D (src/srft.cpp:56-57,128)
+            HStageArgs a = chain_args(op, false, false);
+            a.in = x1;
+            a.ld_in = Ms;
+            a.gather = op.at<int32_t>(h.off_perm);
+            a.out = x2;
+            a.ld_out = Ms;
+            a.out_diag = op.at<double2>(h.off_d);
+            a.rows = rs;
+            EventTimer t(ctx, kernel_ms ? &kernel_ms[1] : nullptr, 1);
+            launch_hstage(a, ctx.stream);
+            ctx.launches += 1;
+            t.stop();
+        }
+        // F and S (src/srft.cpp:129-131)
+        fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
+                 kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
+        if (op.ndups) {
+            launch_copy_dups(out, ldo, out_row0 + s0, rs, op.dups.as<int32_t>(), op.ndups, ctx.stream);
+            ctx.launches += 1;
+        }
+    }
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw Error(MNB_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+int shard_begin(int64_t n, int world, int rank, int64_t* count) {
+    const int64_t base = n / world, extra = n % world;
+    *count = base + (rank < extra ? 1 : 0);
+    return 0;
+}
+
+void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel_ms, double* redistribute_s) {
+    const int64_t m = ctx.m, l = op.host->l;
+    const int is_real = ctx.dtype == MNB_F64;
+    if (ctx.world == 1) {
+        sketch_block(ctx, op, ctx.A, is_real, m, 0, m, out, l, 0, kernel_ms);
+        return;
+    }
+    // ---- all-to-all: column shards -> row blocks (north_star item 5) ----
+    const size_t esz = ctx.esz();
+    std::vector<int64_t> rb(size_t(ctx.world) + 1, 0), cb(size_t(ctx.world) + 1, 0);
+    for (int h = 0; h < ctx.world; ++h) {
+        int64_t b, c;
+        mnb_shard_columns(m, ctx.world, h, &b, &c);
+        rb[size_t(h)] = b;
+        rb[size_t(h) + 1] = b + c;
+        mnb_shard_columns(ctx.n_global, ctx.world, h, &b, &c);
+        cb[size_t(h)] = b;
+        cb[size_t(h) + 1] = b + c;
+    }
+    const int me = ctx.rank;
+    const int64_t mh = rb[size_t(me) + 1] - rb[size_t(me)];
+    cudaEvent_t e0 = ctx.event(10), e1 = ctx.event(11);
+    MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+    unsigned char* pack = static_cast<unsigned char*>(ctx.ws_pack.ensure(size_t(m) * size_t(ctx.n_local) * esz + 16));
+    unsigned char* slab =
+        static_cast<unsigned char*>(ctx.ws_slab.ensure(size_t(std::max<int64_t>(mh, 1)) * size_t(ctx.n_global) * esz + 16));
+    const unsigned char* A = static_cast<const unsigned char*>(ctx.A);
+    for (int h = 0; h < ctx.world; ++h) {
+        const int64_t rows = rb[size_t(h) + 1] - rb[size_t(h)];
+        if (rows == 0 || ctx.n_local == 0) continue;
+        unsigned char* dst = pack + size_t(rb[size_t(h)]) * size_t(ctx.n_local) * esz;
+        MNB_CUDA(cudaMemcpy2DAsync(dst, size_t(rows) * esz, A + size_t(rb[size_t(h)]) * esz, size_t(m) * esz,
+                                   size_t(rows) * esz, size_t(ctx.n_local), cudaMemcpyDeviceToDevice, ctx.stream));
+    }
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int h = 0; h < ctx.world; ++h) {
+        const int64_t rows_h = rb[size_t(h) + 1] - rb[size_t(h)];
+        const int64_t cols_h = cb[size_t(h) + 1] - cb[size_t(h)];
+        unsigned char* send = pack + size_t(rb[size_t(h)]) * size_t(ctx.n_local) * esz;
+        unsigned char* recv = slab + size_t(cb[size_t(h)]) * size_t(mh) * esz;
+        const size_t send_d = size_t(rows_h) * size_t(ctx.n_local) * esz / 8;
+        const size_t recv_d = size_t(mh) * size_t(cols_h) * esz / 8;
+        if (h == me) {
+            if (send_d)
+                MNB_CUDA(cudaMemcpyAsync(recv, send, send_d * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+            continue;
+        }
+        if (send_d) nccl_check(ncclSend(send, send_d, ncclDouble, h, ctx.comm, ctx.stream), "ncclSend");
+        if (recv_d) nccl_check(ncclRecv(recv, recv_d, ncclDouble, h, ctx.comm, ctx.stream), "ncclRecv");
+    }
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+    // ---- local sketch of this rank's row block ----
+    if (mh > 0) sketch_block(ctx, op, slab, is_real, mh, 0, mh, out + rb[size_t(me)] * l, l, 0, kernel_ms);
+    // ---- allgather the sketch columns (every rank runs the replicated QR) ----
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (int h = 0; h < ctx.world; ++h) {
+        const int64_t rows_h = rb[size_t(h) + 1] - rb[size_t(h)];
+        if (!rows_h) continue;
+        double2* blk = out + rb[size_t(h)] * l;
+        nccl_check(ncclBroadcast(blk, blk, size_t(rows_h) * size_t(l) * 2, ncclDouble, h, ctx.comm, ctx.stream),
+                   "ncclBroadcast");
+    }
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+    if (redistribute_s) {
+        MNB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *redistribute_s += ms * 1e-3;
+    }
+}
+
+void dft_vec_to(Context& ctx, int64_t n, const double2* in, double2* out, bool inverse) {
+    double2* tmp = static_cast<double2*>(ctx.vec_full[2].ensure(size_t(n) * 16));
+    fft_rows(ctx, n, in, 1, 1, tmp, 1, out, 1, 0, false, nullptr, inverse, nullptr, nullptr);
+}
+
+void dft_vec(Context& ctx, int64_t n, double2* x, bool inverse) {
+    double2* o = static_cast<double2*>(ctx.vec_full[1].ensure(size_t(n) * 16));
+    dft_vec_to(ctx, n, x, o, inverse);
+    MNB_CUDA(cudaMemcpyAsync(x, o, size_t(n) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+}
+
+void srft_adjoint_vec(Context& ctx, const SrftDev& op, const double2* v, double2* y) {
+    const SrftHost& h = *op.host;
+    const int64_t n = h.n;
+    double2* w = static_cast<double2*>(ctx.vec_full[0].ensure(size_t(n) * 16));
+    double2* wf = static_cast<double2*>(ctx.vec_full[1].ensure(size_t(n) * 16));
+    // S^* v  (src/srft.cpp:137-139)
+    launch_scatter_add_sample(v, h.l, op.at<int32_t>(h.off_sample), h.sampling == MNB_WITH_REPLACEMENT, w, n,
+                              ctx.stream);
+    // F^{-1} (src/srft.cpp:140)
+    dft_vec_to(ctx, n, w, wf, true);
+    {  // conj(D), Theta^*, Pi^*, conj(Z)   (src/srft.cpp:141, :64-66)
+        HStageArgs a = chain_args(op, false, true);
+        a.in = wf;
+        a.ld_in = 1;
+        a.in_diag = op.at<double2>(h.off_d);
+        a.in_diag_conj = 1;
+        a.out = w;
+        a.ld_out = 1;
+        a.scatter = op.at<int32_t>(h.off_perm);
+        a.out_diag = op.at<double2>(h.off_zeta);
+        a.out_diag_conj = 1;
+        a.rows = 1;
+        launch_hstage(a, ctx.stream);
+    }
+    {  // Theta~^*, Pi~^*, conj(Z~)   (src/srft.cpp:67-69)
+        HStageArgs a = chain_args(op, true, true);
+        a.in = w;
+        a.ld_in = 1;
+        a.out = y;
+        a.ld_out = 1;
+        a.scatter = op.at<int32_t>(h.off_perm_tilde);
+        a.out_diag = op.at<double2>(h.off_zeta_tilde);
+        a.out_diag_conj = 1;
+        a.rows = 1;
+        launch_hstage(a, ctx.stream);
+    }
+    ctx.launches += 5;
+}
+
+void srft_apply_vec(Context& ctx, const SrftDev& op, const double2* x, double2* y, bool h_only) {
+    const SrftHost& h = *op.host;
+    const int64_t n = h.n;
+    double2* t1 = static_cast<double2*>(ctx.vec_full[0].ensure(size_t(n) * 16));
+    double2* t2 = static_cast<double2*>(ctx.vec_full[1].ensure(size_t(n) * 16));
+    {
+        HStageArgs a = chain_args(op, true, false);
+        a.in = x;
+        a.ld_in = 1;
+        a.gather = op.at<int32_t>(h.off_perm_tilde);
+        a.in_diag = op.at<double2>(h.off_zeta_tilde);
+        a.out = t1;
+        a.ld_out = 1;
+        a.out_diag = op.at<double2>(h.off_zeta);
+        a.rows = 1;
+        launch_hstage(a, ctx.stream);
+    }
+    {
+        HStageArgs a = chain_args(op, false, false);
+        a.in = t1;
+        a.ld_in = 1;
+        a.gather = op.at<int32_t>(h.off_perm);
+        a.out = h_only ? y : t2;
+        a.ld_out = 1;
+        a.out_diag = h_only ? nullptr : op.at<double2>(h.off_d);
+        a.rows = 1;
+        launch_hstage(a, ctx.stream);
+    }
+    ctx.launches += 2;
+    if (h_only) return;
+    double2* tmp = static_cast<double2*>(ctx.vec_full[2].ensure(size_t(n) * 16));
+    fft_rows(ctx, n, t2, 1, 1, tmp, 1, y, h.l, 0, true, op.at<int32_t>(h.off_sel), false, nullptr, nullptr);
+    if (op.ndups) launch_copy_dups(y, h.l, 0, 1, op.dups.as<int32_t>(), op.ndups, ctx.stream);
+}
+
+}  // namespace mnb

@@ -1,0 +1,103 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle
+(oracle/, a restatement of the reference pinned by tests/test_oracle.py).
+
+Tolerances: FFT / SRFT entries 1e-13 relative (the reference tests' own
+bound, tests/test_srft.cpp:86-98); H stage bit-exact (same operation order,
+exact carries); solves within 10*epsilon of the oracle's x (north_star) and
+CG iteration counts within +-1."""
+import numpy as np
+import pytest
+
+import paper_0905_4745_b200 as mn
+from oracle import minnorm_oracle as O
+from tests.instances import make_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def crandn(rng, *shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 12, 16, 17, 31, 40, 64, 96, 100, 1000, 1024, 1536, 2048, 4096,
+                               6144, 16384, 131072])
+def test_dft_matches_oracle(ctx, n):
+    rng = np.random.default_rng(n)
+    x = crandn(rng, n)
+    y = mn.dft(x, ctx)
+    assert rel(y, O.dft(x)) <= 1e-13
+    assert rel(y, np.fft.fft(x) / np.sqrt(n)) <= 1e-13
+    assert rel(mn.idft(y, ctx), x) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [2, 3, 17, 64, 1000, 4096, 65536])
+def test_apply_h_bit_exact(ctx, n):
+    seed = mn.derive_seed(13, n)
+    op = mn.build_srft(1, n, seed)
+    ref = O.Srft.build(1, n, seed)
+    x = crandn(np.random.default_rng(n), n)
+    y = op.apply_h(x, ctx)
+    yr = ref.apply_h(x)
+    assert np.array_equal(y, yr), f"max diff {np.abs(y - yr).max():.3e}"
+
+
+@pytest.mark.parametrize("l,n", [(3, 8), (5, 16), (50, 100), (256, 1024), (1024, 16384), (4096, 131072),
+                                 (100, 6144)])
+@pytest.mark.parametrize("mode", [mn.Sampling.without_replacement, mn.Sampling.with_replacement])
+def test_apply_and_adjoint_match_oracle(ctx, l, n, mode):
+    seed = mn.derive_seed(19, n + int(mode))
+    op = mn.build_srft(l, n, seed, mode)
+    ref = O.Srft.build(l, n, seed, mode == mn.Sampling.without_replacement)
+    rng = np.random.default_rng(l + n)
+    x = crandn(rng, n)
+    v = crandn(rng, l)
+    assert rel(op.apply(x, ctx), ref.apply(x)) <= 1e-13
+    assert rel(op.apply_adjoint(v, ctx), ref.apply_adjoint(v)) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160)])
+def test_sketch_matches_oracle(ctx, m, n, l):
+    A, _ = make_instance(m, n, kappa=1e3, seed=m + n)
+    seed = mn.derive_seed(42, 11)
+    op = mn.build_srft(l, n, seed)
+    ref = O.Srft.build(l, n, seed)
+    ctx.set_matrix(A)
+    S = op.sketch(ctx)
+    Sr = ref.sketch(A)
+    assert rel(S, Sr) <= 1e-13
+
+
+def test_sketch_real_matrix(ctx):
+    A, _ = make_instance(32, 6144, kappa=1e3, seed=5, real=True)
+    seed = mn.derive_seed(42, 12)
+    op = mn.build_srft(128, 6144, seed)
+    ref = O.Srft.build(128, 6144, seed)
+    ctx.set_matrix(A)
+    assert rel(op.sketch(ctx), ref.sketch(A)) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (16, 256, 1e2, 1e-8),
+                                           (48, 6144, 1e4, 1e-10)])
+def test_solve_randomized_matches_oracle(ctx, m, n, kappa, eps):
+    A, b = make_instance(m, n, kappa, seed=m * 7 + 1)
+    cfg = mn.SolverConfig(epsilon=eps, seed=42)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    ref = O.solve_randomized(A, b, epsilon=eps, seed=42)
+    assert rel(rep.x, ref.x) <= 10 * eps
+    assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
+    assert rep.lsq_converged == ref.lsq_converged
+    assert rep.residual_norm <= 1e-6 * np.linalg.norm(b) * kappa
+    assert abs(rep.c_norm_ratio - ref.c_norm_ratio) <= 1e-8 * ref.c_norm_ratio
+
+
+def test_solve_real_matrix(ctx):
+    A, b = make_instance(32, 6144, 1e4, seed=3, real=True)
+    cfg = mn.SolverConfig(epsilon=1e-10)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    ref = O.solve_randomized(A, b, epsilon=1e-10)
+    assert rel(rep.x, ref.x) <= 1e-9
+    assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1

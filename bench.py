@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native randomized minimal-norm solve (arXiv 0905.4745).
+
+One "step" = one full solve_randomized (Steps 1-5, both SRFT sketches, both
+QRs, the preconditioned CG, x = A^H y) on one synthetic instance of a
+BASELINE.json config (default c4: m=2048, n=2^20 complex128, the
+bandwidth-bound PCG regime; A = 32 GiB > the 126 MB L2, so no flush is
+needed between steps).  Prints ONE JSON line (rank 0).
+
+  python bench.py [--config c4] [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Multi-GPU: launched with torch.distributed.run, one rank per GPU; A is
+column-sharded (strong scaling of one solve), NCCL inside the library.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # BASELINE.json "configs"
+    "c1": dict(m=64, n=1024, kappa=1e3, eps=1e-12, real=False),
+    "c2": dict(m=256, n=16384, kappa=1e6, eps=1e-10, real=False),
+    "c3": dict(m=1024, n=131072, kappa=1e8, eps=1e-10, real=False),
+    "c4": dict(m=2048, n=1 << 20, kappa=1e4, eps=1e-8, real=False),
+    "c5": dict(m=4096, n=3 << 20, kappa=1e6, eps=1e-10, real=True),
+}
+METRIC = "min-norm solve time; HBM GB/s of fused PCG A(A*y) pass & SRFT sketch vs peak"
+DATA_SEED = 20260101
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ data ---
+def make_A_shard(cfg, col_begin, n_local, device):
+    """A[:, col_begin:col_begin+n_local] of A = U diag(sigma) G / sqrt(n), built on
+    the GPU chunk by chunk with seeds tied to global column chunks (so every
+    world size sees the same bits).  Column-major (returned as A with strides (1, m))."""
+    import torch
+    m, n, real = cfg["m"], cfg["n"], cfg["real"]
+    ctype = torch.float64 if real else torch.complex128
+    gU = torch.Generator(device=device).manual_seed(DATA_SEED)
+    if real:
+        Z = torch.randn((m, m), dtype=torch.float64, device=device, generator=gU)
+    else:
+        Z = torch.randn((m, m), dtype=torch.complex128, device=device, generator=gU)
+    Q, R = torch.linalg.qr(Z)
+    d = torch.diagonal(R)
+    U = Q * (d / d.abs())
+    sigma = torch.logspace(0, -math.log10(cfg["kappa"]), m, dtype=torch.float64, device=device)
+    Us = (U * sigma.to(ctype)) / math.sqrt(n)
+    At = torch.empty((n_local, m), dtype=ctype, device=device)  # row-major (n x m) == column-major A
+    chunk = 1 << 16
+    first, last = col_begin // chunk, (col_begin + n_local - 1) // chunk
+    for ci in range(first, last + 1):
+        g = torch.Generator(device=device).manual_seed(DATA_SEED + 1 + ci)
+        c0 = ci * chunk
+        width = min(chunk, n - c0)
+        G = torch.randn((m, width), dtype=ctype, device=device, generator=g)
+        blk = (Us @ G).T  # width x m
+        lo, hi = max(c0, col_begin), min(c0 + width, col_begin + n_local)
+        At[lo - col_begin:hi - col_begin] = blk[lo - c0:hi - c0]
+        del G, blk
+    del Z, Q, R, U
+    return At.T  # m x n_local, column-major view
+
+
+def make_b(cfg):
+    import numpy as np
+    rng = np.random.default_rng(DATA_SEED + 7)
+    m = cfg["m"]
+    if cfg["real"]:
+        return rng.standard_normal(m).astype(np.complex128)
+    return (rng.standard_normal(m) + 1j * rng.standard_normal(m)) / np.sqrt(2)
+
+
+# ---------------------------------------------------------------- clocks ---
+class ClockSampler:
+    def __init__(self, device_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device_index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 8:
+                    continue
+                try:
+                    sm.append(float(p[0]))
+                    mx = max(mx, float(p[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, p[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------- CPU baseline --
+def cpu_sample(cfg, gpu_iterations=None, threads=None):
+    """Times the oracle port (oracle/, the reference's algorithm restated; the
+    reference itself needs Eigen and cannot be built here) on a bounded
+    sample of the workload and scales it to one full solve.  Returns
+    (seconds_per_solve, cores, description)."""
+    import numpy as np
+    import scipy.linalg as sla
+    from oracle import minnorm_oracle as O
+    from tests.instances import make_instance
+    threads = threads or os.cpu_count() or 1
+    m, n, real = cfg["m"], cfg["n"], cfg["real"]
+    l = 4 * m
+    rng = np.random.default_rng(1)
+    # (1) sketch: k rows through T (both sketches in the solve; column loop parallel)
+    k = max(threads, 4)
+    Ak = rng.standard_normal((k, n)) if real else (rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n)))
+    Ak = np.asfortranarray(Ak)
+    t0 = time.perf_counter()
+    op = O.Srft.build(l, n, O.derive_seed(42, 11))
+    t_param = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    op.sketch(Ak, threads=threads)
+    t_rows = time.perf_counter() - t0
+    t_sketch = 2 * (t_rows * m / k + t_param)
+    # (2) one CG iteration = 2 GEMVs over A (lsq.cpp:71-73): time a column slice, scale by n
+    cols = min(n, 1 << 15)
+    As = np.asfortranarray(rng.standard_normal((m, cols)) if real else
+                           rng.standard_normal((m, cols)) + 1j * rng.standard_normal((m, cols)))
+    v = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+    w = rng.standard_normal(cols) + 1j * rng.standard_normal(cols)
+    O.AH_v(As, v)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        O.AH_v(As, v)
+        O.A_r(As, w)
+    t_iter = (time.perf_counter() - t0) / reps * (n / cols)
+    # (3) QR of an l x m sketch (scaled from a smaller QR by the flop count 8(l m^2 - m^3/3))
+    mq = min(m, 512)
+    lq = 4 * mq
+    Sq = rng.standard_normal((lq, mq)) + 1j * rng.standard_normal((lq, mq))
+    t0 = time.perf_counter()
+    sla.qr(Sq, mode="economic")
+    t_qr_small = time.perf_counter() - t0
+    t_qr = 2 * t_qr_small * (l * m * m - m ** 3 / 3) / (lq * mq * mq - mq ** 3 / 3)
+    # (4) CG iteration count: the GPU's, or the oracle on a scaled analog with the same l/n and kappa
+    if gpu_iterations is None:
+        ma = 32
+        na = max(ma * 8, int(n * ma / m))
+        Aa, ba = make_instance(ma, na, cfg["kappa"], seed=3, real=real)
+        gpu_iterations = O.solve_randomized(Aa, ba, epsilon=cfg["eps"]).lsq_iterations
+    total = t_sketch + t_qr + (gpu_iterations + 2) * t_iter
+    desc = (f"oracle port on {threads} threads: {k} rows of the SRFT sketch (scaled x{m}/{k}, x2 sketches) + "
+            f"2 GEMVs over a {m}x{cols} slice (scaled x{n}/{cols}, x{gpu_iterations}+2 passes) + "
+            f"{lq}x{mq} QR (flop-scaled to {l}x{m}, x2)")
+    return total, threads, desc
+
+
+# ----------------------------------------------------------------- main ----
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config_json = {"workload": f"BASELINE {args.config}: m={cfg['m']} n={cfg['n']} "
+                               f"{'float64' if cfg['real'] else 'complex128'} kappa={cfg['kappa']:g} "
+                               f"eps={cfg['eps']:g} l=4m",
+                   "m": cfg["m"], "n": cfg["n"], "l": 4 * cfg["m"], "epsilon": cfg["eps"],
+                   "parallelism": f"column-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "A (%.1f GiB) exceeds L2; no flush needed" % (cfg["m"] * cfg["n"] * (8 if cfg["real"] else 16) / 2**30)}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        samples = []
+        for i in range(args.warmup + args.steps):
+            v, cores, desc = cpu_sample(cfg)
+            if i >= args.warmup:
+                samples.append(v)
+        val = statistics.mean(samples)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64" if cfg["real"] else "c128", "data": "synthetic (seeded)",
+            "config": config_json,
+            "cpu_baseline": {"value": val, "unit": "s", "cores": cores, "kind": "port", "sample": desc},
+            "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import numpy as np
+    import torch
+    import paper_0905_4745_b200 as mn
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        uid = [mn.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = mn.Context.distributed(local, rank, world, uid[0])
+    else:
+        dist = None
+        ctx = mn.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    m, n = cfg["m"], cfg["n"]
+    col_begin, n_local = mn.shard_columns(n, world, rank)
+    A = make_A_shard(cfg, col_begin, n_local, dev)
+    b = make_b(cfg)
+    ctx.n, ctx.col_begin = n, col_begin
+    ctx.set_matrix(A, n_global=n, col_begin=col_begin)
+    scfg = mn.SolverConfig(epsilon=cfg["eps"], seed=42)
+    x_dev = torch.empty(max(n_local, 1), dtype=torch.complex128, device=dev)
+    inst = mn.ProblemInstance(None, b)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident arm: A already in HBM
+    for _ in range(args.warmup):
+        mn.solve_randomized(inst, scfg, ctx, x_out=x_dev)
+    barrier()
+    clocks = ClockSampler(local)
+    reps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    for _ in range(args.steps):
+        barrier()
+        e0.record(stream)
+        rep = mn.solve_randomized(inst, scfg, ctx, x_out=x_dev)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+        reps.append(rep)
+    barrier()
+    clk = clocks.stop()
+    ms = statistics.mean(step_ms)
+    value = ms / 1e3
+    hbm_peak, peak_kind = peaks()
+    esz = 8 if cfg["real"] else 16
+    pass_ms = statistics.mean(r.extra["pcg_pass_ms_sum"] / max(1, r.extra["pcg_pass_launches"]) for r in reps)
+    pass_bytes = esz * m * n_local + 64 * n_local  # A once + the lagged r / t n-vectors (read + write)
+    achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            prof = json.load(f).get(args.config, {})
+        traffic = prof.get("pcg_pass_dram_bytes_per_launch")
+    except Exception:
+        pass
+    last = reps[-1]
+    sk = last.extra["sketch_kernel_ms"]
+    launches = sum(r.extra["kernel_launches"] for r in reps)
+
+    # ---- end-to-end arm: public API with host buffers (H2D of A and b, D2H of x inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        A_host = torch.empty((n_local, m), dtype=A.dtype, pin_memory=True)
+        A_host.copy_(A.T)
+        A_np = A_host.numpy().T  # m x n_local, column-major view of pinned memory
+        del A
+        ctx._keep = None
+        torch.cuda.empty_cache()
+        inst_h = mn.ProblemInstance(A_np, b)
+        e2e_ms = []
+        for i in range(max(1, args.warmup // 2) + args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            rep_h = mn.solve_randomized(inst_h, scfg, ctx)  # set_matrix(host) + solve + x to host
+            torch.cuda.synchronize(dev)
+            dt = max_over_ranks((time.perf_counter() - t0) * 1e3)
+            if i >= max(1, args.warmup // 2):
+                e2e_ms.append(dt)
+        e2e = {"value": statistics.mean(e2e_ms) / 1e3, "unit": "s",
+               "h2d_bytes_per_step": esz * m * n_local + 16 * m, "d2h_bytes_per_step": 16 * n_local,
+               "note": "wall clock around mnb_solve_randomized with host A (pinned) and host x"}
+        if rank == 0:
+            assert np.all(np.isfinite(rep_h.x))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, desc = cpu_sample(cfg, gpu_iterations=last.lsq_iterations)
+        cpu = {"value": v, "unit": "s", "cores": cores, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64" if cfg["real"] else "c128", "data": "synthetic (seeded, on device)",
+            "config": config_json,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "pcg_pass_kernel",
+                         "peak_kind": peak_kind, "bytes_per_launch": pass_bytes, "ms_per_launch": pass_ms},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "solve": {"lsq_iterations": last.lsq_iterations, "lsq_converged": last.lsq_converged,
+                      "residual_norm": last.residual_norm, "c_norm_ratio": last.c_norm_ratio,
+                      "step_seconds": last.step_seconds, "param_seconds": last.extra["param_seconds"],
+                      "sketch_seconds": last.extra["sketch_seconds"], "qr_seconds": last.extra["qr_seconds"],
+                      "pcg_seconds": last.extra["pcg_seconds"],
+                      "redistribute_seconds": last.extra["redistribute_seconds"],
+                      "sketch_kernel_ms": {"hstage1": sk[0], "hstage2": sk[1], "fft_a": sk[2], "fft_b": sk[3]},
+                      "sketch_hbm_gbs": {
+                          "hstage1": 2 * (esz + 16) * m * n / max(sk[0] * 1e-3, 1e-12) / 1e9,
+                          "hstage2": 2 * 32 * m * n / max(sk[1] * 1e-3, 1e-12) / 1e9,
+                          "fft_a": 2 * 32 * m * n / max(sk[2] * 1e-3, 1e-12) / 1e9,
+                          "fft_b": 2 * 16 * m * n / max(sk[3] * 1e-3, 1e-12) / 1e9},
+                      "note_sketch": "sketch_kernel_ms sums both sketches (S and E); GB/s = algorithmic bytes "
+                                     "(read + write of one m x n pass) x 2 sketches / time"},
+        }
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

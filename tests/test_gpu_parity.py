@@ -80,18 +80,36 @@ def test_sketch_real_matrix(ctx):
     assert rel(op.sketch(ctx), ref.sketch(A)) <= 1e-13
 
 
+EPS_MACH = np.finfo(float).eps
+
+
+def solve_tol(eps, kappa):
+    """What a backward-stable solver can promise: 10*eps (north_star), but not
+    below the conditioning floor ~ eps_mach * kappa (SURVEY §8c measured
+    6e-9 between two exact solvers at kappa = 1e8)."""
+    return max(10 * eps, 10 * EPS_MACH * kappa)
+
+
 @pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (16, 256, 1e2, 1e-8),
-                                           (48, 6144, 1e4, 1e-10)])
+                                           (48, 6144, 1e4, 1e-10), (128, 32768, 1e4, 1e-8)])
 def test_solve_randomized_matches_oracle(ctx, m, n, kappa, eps):
     A, b = make_instance(m, n, kappa, seed=m * 7 + 1)
     cfg = mn.SolverConfig(epsilon=eps, seed=42)
     rep = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    p = O.solve_classical(A, b)  # exact minimal-norm solution (pivoted QR, src/solver.cpp:130-146)
+    assert rel(rep.x, p) <= solve_tol(eps, kappa)
+    assert rep.lsq_converged
     ref = O.solve_randomized(A, b, epsilon=eps, seed=42)
-    assert rel(rep.x, ref.x) <= 10 * eps
-    assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
-    assert rep.lsq_converged == ref.lsq_converged
+    if ref.lsq_converged:
+        # the reference converged: match its x and its iteration count
+        assert rel(rep.x, ref.x) <= 10 * eps + 2 * rel(ref.x, p)
+        assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
+        assert abs(rep.c_norm_ratio - ref.c_norm_ratio) <= 1e-8 * ref.c_norm_ratio
+    else:
+        # the reference's stop rule is below its own gradient floor (eps_mach*kappa)^2 > tau:
+        # it runs lsq_max_iterations and diverges (DESIGN.md "Where the reference cannot converge")
+        assert ref.lsq_iterations == 300
     assert rep.residual_norm <= 1e-6 * np.linalg.norm(b) * kappa
-    assert abs(rep.c_norm_ratio - ref.c_norm_ratio) <= 1e-8 * ref.c_norm_ratio
 
 
 def test_solve_real_matrix(ctx):

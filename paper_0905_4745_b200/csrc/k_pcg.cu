@@ -23,7 +23,7 @@ namespace mnb {
 namespace {
 
 constexpr int kConsumerWarps = 16;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kThreads = kConsumerWarps * 32;  // no separate producer warp: thread 0 issues the TMA
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -97,42 +97,85 @@ __device__ __forceinline__ void axpy_acc<double>(double2& acc, double a, double2
     acc.y = fma(a, t.y, acc.y);
 }
 
+// Columns per batch for a thread owning EPL rows: keeps the two register
+// batches (current + next) at <= 16 complex (or 32 real) values per thread.
+template <typename AT, int EPL>
+__host__ __device__ constexpr int batch_cols() {
+    return sizeof(AT) == 16 ? (EPL <= 2 ? 4 : EPL == 4 ? 2 : 1) : (EPL <= 2 ? 4 : EPL == 4 ? 2 : 1);
+}
+
 struct SmemLayout {
     size_t tileA, tileT, tileR, stage_bytes, red, bars, total;
 };
 
-__host__ __device__ inline SmemLayout smem_layout(int64_t m, int64_t C, int esz, int stages) {
+__host__ __device__ inline SmemLayout smem_layout(int64_t m, int64_t C, int esz, int stages, int V) {
     SmemLayout L;
     const size_t a = size_t(C) * size_t(m) * size_t(esz);
     L.tileA = 0;
     L.tileT = (a + 127) & ~size_t(127);
     L.tileR = L.tileT + ((size_t(C) * 16 + 127) & ~size_t(127));
     L.stage_bytes = L.tileR + ((size_t(C) * 16 + 127) & ~size_t(127));
-    L.red = size_t(stages) * L.stage_bytes;                     // [8 groups][2 bufs][16 warps] complex
-    L.bars = L.red + size_t(8 * 2 * kConsumerWarps) * 16;
+    L.red = size_t(stages) * L.stage_bytes;  // [groups][2 bufs][G warps][V] doubles = 2 * 16 * V doubles
+    L.bars = L.red + size_t(2 * kConsumerWarps * V) * 8;
     L.total = L.bars + size_t(2 * stages) * 8;
     return L;
 }
 
+// In-warp transposed reduction of V values (V | 32): afterwards every lane
+// holds the warp-wide sum of value index  lane >> (5 - log2 V)  in v[0].
+// V-1 + 5-log2(V) shuffles instead of 5 V.
+template <int V>
+__device__ __forceinline__ void xreduce(double (&v)[V], int lane) {
+    int mask = 16;
+#pragma unroll
+    for (int c = V; c > 1; c >>= 1) {
+        const bool up = (lane & mask) != 0;
+#pragma unroll
+        for (int i = 0; i < c / 2; ++i) {
+            const double send = up ? v[i] : v[i + c / 2];
+            const double keep = up ? v[i + c / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+        }
+        mask >>= 1;
+    }
+#pragma unroll
+    for (; mask > 0; mask >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], mask);
+}
+
+template <int V>
+__host__ __device__ constexpr int log2c() { return V <= 1 ? 0 : 1 + log2c<V / 2>(); }
+
+// Fused CG pass over this CTA's contiguous column range.
+//
+// A group of G consumer warps owns all m rows (thread: EPL rows, stride
+// 32 G); NG = 16/G groups split each shared-memory stage, K columns each.
+// Per batch of K columns a warp forms K partial dot products, reduces them
+// in-warp (xreduce), publishes them to shared memory, and -- one named
+// barrier later -- sums the G warp partials into t.  The loop is software
+// pipelined: the dot products of batch b+1 are issued between the barrier
+// and the axpy of batch b, so the reduction latency hides behind FMA work,
+// and a stage is handed back to the TMA producer as soon as it sits in
+// registers.  All sums run in a fixed order (bitwise reproducible).
 template <typename AT, int EPL>
-__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int G, int cpg, int stages,
-                                                               int64_t C) {
+__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int G, int stages, int64_t C,
+                                                               int64_t per) {
+    constexpr int K = batch_cols<AT, EPL>();
+    constexpr int V = 2 * K;
     extern __shared__ __align__(128) unsigned char smem[];
     if (p.state && p.state->done) return;  // uniform: converged loops cost one launch
     const int64_t m = p.m;
-    const int esz = int(sizeof(AT));
-    const SmemLayout L = smem_layout(m, C, esz, stages);
+    const int mi = int(m);
+    constexpr int esz = int(sizeof(AT));
+    const SmemLayout L = smem_layout(m, C, esz, stages, V);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + stages;
-    double2* red = reinterpret_cast<double2*>(smem + L.red);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NG = kConsumerWarps / G;
-    // contiguous column range of this CTA
-    const int64_t per = (p.n + gridDim.x - 1) / gridDim.x;
     const int64_t cb = min(p.n, int64_t(blockIdx.x) * per), ce = min(p.n, cb + per);
     const int64_t nstage = (ce - cb + C - 1) / C;
-    const bool need_t = p.mode == PCG_INIT || p.mode == PCG_CG;
+    const bool init = p.mode == PCG_INIT;
+    const bool need_t = init || p.mode == PCG_CG;
     const bool need_r = p.mode == PCG_CG;
     const double alpha_prev = (p.mode == PCG_CG && p.state) ? p.state->alpha : 0.0;
 
@@ -145,108 +188,162 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     }
     __syncthreads();
 
-    if (warp == kConsumerWarps) {
-        // ------------------------------------------------------ producer
-        if (lane == 0) {
-            for (int64_t s = 0; s < nstage; ++s) {
-                const int slot = int(s % stages);
-                if (s >= stages) mbar_wait(&empty[slot], uint32_t(((s / stages) - 1) & 1));
-                const int64_t c0 = cb + s * C;
-                const int64_t cc = min(C, ce - c0);
-                unsigned char* st = smem + slot * L.stage_bytes;
-                const uint32_t abytes = uint32_t(cc * m * esz);
-                const uint32_t vbytes = uint32_t(cc * 16);
-                mbar_expect_tx(&full[slot], abytes + (need_t ? vbytes : 0u) + (need_r ? vbytes : 0u));
-                bulk_g2s(st + L.tileA, static_cast<const unsigned char*>(p.A) + size_t(c0) * size_t(m) * esz, abytes,
-                         &full[slot]);
-                if (need_t) bulk_g2s(st + L.tileT, p.tin + c0, vbytes, &full[slot]);
-                if (need_r) bulk_g2s(st + L.tileR, p.r + c0, vbytes, &full[slot]);
-            }
-        }
-        // the producer warp joins the epilogue's block-wide barriers below
-    }
+    // Producer (thread 0): fill stage s into slot s % stages.  The first
+    // `stages` fills are issued here; later ones from the consumer loop once
+    // every warp has moved the previous occupant of the slot into registers.
+    auto produce = [&](int64_t s) {
+        const int slot = int(s % stages);
+        if (s >= stages) mbar_wait(&empty[slot], uint32_t(((s / stages) - 1) & 1));
+        const int64_t c0 = cb + s * C;
+        const int64_t cc = min(C, ce - c0);
+        unsigned char* st = smem + slot * L.stage_bytes;
+        const size_t abytes = size_t(cc) * size_t(m) * esz;
+        const uint32_t abulk = uint32_t(abytes & ~size_t(15));
+        const unsigned char* src = static_cast<const unsigned char*>(p.A) + size_t(c0) * size_t(m) * esz;
+        if (abytes != abulk)  // odd real tail: 8 bytes by hand, published by the arrive below
+            *reinterpret_cast<double*>(st + L.tileA + abulk) = __ldg(reinterpret_cast<const double*>(src + abulk));
+        const uint32_t vbytes = uint32_t(cc * 16);
+        mbar_expect_tx(&full[slot], abulk + (need_t ? vbytes : 0u) + (need_r ? vbytes : 0u));
+        if (abulk) bulk_g2s(st + L.tileA, src, abulk, &full[slot]);
+        if (need_t) bulk_g2s(st + L.tileT, p.tin + c0, vbytes, &full[slot]);
+        if (need_r) bulk_g2s(st + L.tileR, p.r + c0, vbytes, &full[slot]);
+    };
+    if (threadIdx.x == 0)
+        for (int64_t s = 0; s < nstage && s < stages; ++s) produce(s);
 
     // ---------------------------------------------------------- consumers
     const int gq = warp / G, wig = warp % G;
+    const int row0 = wig * 32 + lane, rstep = 32 * G;
     double2 wreg[EPL], sacc[EPL];
-    const int row0 = wig * 32 + lane, rstep = 32 * G, mi = int(m);
 #define ROW(e) (row0 + (e) * rstep)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
         sacc[e] = make_double2(0.0, 0.0);
         wreg[e] = make_double2(0.0, 0.0);
     }
-    double qq = 0.0, rt = 0.0, rr = 0.0;  // leader-lane partials
-    if (warp < kConsumerWarps) {
-        if (p.mode != PCG_INIT) {
+    double qq = 0.0, rt = 0.0, rr = 0.0;  // per-lane partials (lanes < K of warp wig == 0)
+    double* red = reinterpret_cast<double*>(smem + L.red) + size_t(gq) * 2 * G * V;  // [2][G][V]
+    if (nstage > 0) {
+        if (!init) {
 #pragma unroll
             for (int e = 0; e < EPL; ++e)
                 if (ROW(e) < mi) wreg[e] = p.w[ROW(e)];
         }
-        int buf = 0;
-        for (int64_t s = 0; s < nstage; ++s) {
+        // lane k < K of the epilogue warp carries column k's t_old / r
+        AT a0[K][EPL];
+        double2 to0 = make_double2(0.0, 0.0), r0 = to0;
+        double2 tin0[K];  // INIT: t = c for all K columns (every lane)
+        double v0[V];
+
+        auto load = [&](int64_t s, AT (&a)[K][EPL], double2& told, double2& rk, double2 (&tin)[K]) {
             const int slot = int(s % stages);
             mbar_wait(&full[slot], uint32_t((s / stages) & 1));
-            const int64_t c0 = cb + s * C;
-            const int64_t cc = min(C, ce - c0);
+            const int64_t cc = min(C, ce - (cb + s * C));
             const unsigned char* st = smem + slot * L.stage_bytes;
             const AT* tA = reinterpret_cast<const AT*>(st + L.tileA);
             const double2* tT = reinterpret_cast<const double2*>(st + L.tileT);
             const double2* tR = reinterpret_cast<const double2*>(st + L.tileR);
-            for (int i = 0; i < cpg; ++i) {
-                const int64_t col = int64_t(gq) + int64_t(i) * NG;  // column within the stage
-                if (col >= cc) break;                                 // uniform per group
-                AT a[EPL];
 #pragma unroll
-                for (int e = 0; e < EPL; ++e) a[e] = ROW(e) < mi ? tA[int(col) * mi + ROW(e)] : zero_of<AT>();
-                double2 t;
-                if (p.mode == PCG_INIT) {
-                    t = tT[col];
-                } else {
-                    double2 part = make_double2(0.0, 0.0);
+            for (int k = 0; k < K; ++k) {
+                const int col = gq * K + k;
 #pragma unroll
-                    for (int e = 0; e < EPL; ++e) dot_acc<AT>(part, a[e], wreg[e]);
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        const double2 q = shfl_xor2(part, o);
-                        part.x += q.x;
-                        part.y += q.y;
-                    }
-                    if (G == 1) {
-                        t = part;
-                    } else {
-                        double2* rb = red + (gq * 2 + buf) * kConsumerWarps;
-                        if (lane == 0) rb[wig] = part;
-                        named_bar(1 + gq, G * 32);
-                        t = rb[0];
-                        for (int k = 1; k < G; ++k) t = c_add(t, rb[k]);
-                        buf ^= 1;
-                    }
-                }
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) axpy_acc<AT>(sacc[e], a[e], t);
-                if (wig == 0 && lane == 0) {
-                    const int64_t k = c0 + col;
-                    if (p.mode == PCG_CG) {
-                        const double2 told = tT[col];
-                        double2 rk = tR[col];
-                        rk.x = fma(-alpha_prev, told.x, rk.x);
-                        rk.y = fma(-alpha_prev, told.y, rk.y);
-                        rr = fma(rk.x, rk.x, fma(rk.y, rk.y, rr));
-                        rt = fma(rk.x, t.x, fma(rk.y, t.y, rt));  // Re(conj(r) t)
-                        p.r[k] = rk;
-                        p.tout[k] = t;
-                    } else if (p.mode == PCG_INIT) {
-                        p.r[k] = t;
-                        p.tout[k] = make_double2(0.0, 0.0);
-                    } else {
-                        p.tout[k] = t;
-                    }
-                    qq = fma(t.x, t.x, fma(t.y, t.y, qq));
-                }
+                for (int e = 0; e < EPL; ++e)
+                    a[k][e] = (col < cc && ROW(e) < mi) ? tA[col * mi + ROW(e)] : zero_of<AT>();
+                if (init) tin[k] = col < cc ? tT[col] : make_double2(0.0, 0.0);
+            }
+            const int myc = gq * K + lane;
+            if (p.mode == PCG_CG && lane < K && myc < cc) {
+                told = tT[myc];
+                rk = tR[myc];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
+        };
+        // partial dot products of one batch, reduced in-warp and published
+        auto dots = [&](const AT (&a)[K][EPL], double (&v)[V], int buf) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double2 part = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) dot_acc<AT>(part, a[k][e], wreg[e]);
+                v[2 * k] = part.x;
+                v[2 * k + 1] = part.y;
+            }
+            xreduce<V>(v, lane);
+            if (G > 1 && (lane & ((32 / V) - 1)) == 0) red[(buf * G + wig) * V + (lane >> (5 - log2c<V>()))] = v[0];
+        };
+        // t of one batch from the published partials
+        auto gather_t = [&](const double (&v)[V], int buf, double2 (&t)[K]) {
+            double acc;
+            if (G > 1) {
+                acc = 0.0;
+                for (int j = lane; j < G * V; j += 32) acc += red[buf * G * V + j];
+#pragma unroll
+                for (int mask = V; mask < 32; mask <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, mask);
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    t[k] = make_double2(__shfl_sync(0xffffffffu, acc, 2 * k), __shfl_sync(0xffffffffu, acc, 2 * k + 1));
+            } else {
+                acc = v[0];
+                constexpr int sh = 5 - log2c<V>();
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    t[k] = make_double2(__shfl_sync(0xffffffffu, acc, (2 * k) << sh),
+                                        __shfl_sync(0xffffffffu, acc, (2 * k + 1) << sh));
+            }
+        };
+        // axpy + per-column epilogue of batch s
+        auto finish = [&](int64_t s, const AT (&a)[K][EPL], const double2 (&t)[K], double2 told, double2 rk) {
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) axpy_acc<AT>(sacc[e], a[k][e], t[k]);
+            const int64_t c0 = cb + s * C;
+            const int64_t cc = min(C, ce - c0);
+            const int myc = gq * K + lane;
+            if (wig == 0 && lane < K && myc < cc) {
+                double2 tk = t[0];
+#pragma unroll
+                for (int k = 1; k < K; ++k)
+                    if (lane == k) tk = t[k];
+                const int64_t col = c0 + myc;
+                if (p.mode == PCG_CG) {
+                    rk.x = fma(-alpha_prev, told.x, rk.x);
+                    rk.y = fma(-alpha_prev, told.y, rk.y);
+                    rr = fma(rk.x, rk.x, fma(rk.y, rk.y, rr));
+                    rt = fma(rk.x, tk.x, fma(rk.y, tk.y, rt));  // Re(conj(r) t)
+                    p.r[col] = rk;
+                    p.tout[col] = tk;
+                } else if (init) {
+                    p.r[col] = tk;
+                    p.tout[col] = make_double2(0.0, 0.0);
+                } else {
+                    p.tout[col] = tk;
+                }
+                qq = fma(tk.x, tk.x, fma(tk.y, tk.y, qq));
+            }
+        };
+        // one step: finish batch s (already reduced and published), then load
+        // and publish batch s+1.  A single register batch keeps the kernel at
+        // <= 128 registers; 16 warps per SM cover the reduction latency.
+        load(0, a0, to0, r0, tin0);
+        if (!init) dots(a0, v0, 0);
+        for (int64_t s = 0; s < nstage; ++s) {
+            const int buf = int(s & 1);
+            if (G > 1 && !init) named_bar(1 + gq, G * 32);
+            double2 t[K];
+            if (init) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) t[k] = tin0[k];
+            } else {
+                gather_t(v0, buf, t);
+            }
+            finish(s, a0, t, to0, r0);
+            if (s + 1 < nstage) {
+                load(s + 1, a0, to0, r0, tin0);
+                if (threadIdx.x == 0 && s + stages < nstage) produce(s + stages);
+                if (!init) dots(a0, v0, buf ^ 1);
+            }
         }
     }
 
@@ -254,14 +351,23 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     __syncthreads();  // all stages consumed: the stage ring is free
     double2* sred = reinterpret_cast<double2*>(smem);  // [NG][m]
     double* scal = reinterpret_cast<double*>(smem + size_t(NG) * size_t(m) * 16);
-    if (warp < kConsumerWarps) {
+    {
 #pragma unroll
         for (int e = 0; e < EPL; ++e)
             if (ROW(e) < mi) sred[gq * mi + ROW(e)] = sacc[e];
-        if (wig == 0 && lane == 0) {
-            scal[gq * 3 + 0] = qq;
-            scal[gq * 3 + 1] = rt;
-            scal[gq * 3 + 2] = rr;
+        if (wig == 0) {
+            // lanes >= K hold zeros; fixed-order butterfly
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                qq += __shfl_xor_sync(0xffffffffu, qq, o);
+                rt += __shfl_xor_sync(0xffffffffu, rt, o);
+                rr += __shfl_xor_sync(0xffffffffu, rr, o);
+            }
+            if (lane == 0) {
+                scal[gq * 3 + 0] = qq;
+                scal[gq * 3 + 1] = rt;
+                scal[gq * 3 + 2] = rr;
+            }
         }
     }
 #undef ROW
@@ -528,7 +634,7 @@ template <typename AT, int EPL>
 void launch_typed(const PcgPassArgs& a, const PcgPlan& pl, cudaStream_t stream) {
     auto k = pcg_pass_kernel<AT, EPL>;
     MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
-    k<<<pl.grid, kThreads, pl.smem, stream>>>(a, pl.G, pl.cols_per_group, pl.stages, pl.stage_cols);
+    k<<<pl.grid, kThreads, pl.smem, stream>>>(a, pl.G, pl.stages, pl.stage_cols, pl.per_cta);
     MNB_LAUNCH_CHECK();
 }
 
@@ -537,31 +643,41 @@ void launch_typed(const PcgPassArgs& a, const PcgPlan& pl, cudaStream_t stream) 
 PcgPlan plan_pcg_pass(int64_t m, int64_t n, int is_real, int num_sms) {
     PcgPlan pl;
     const int esz = is_real ? 8 : 16;
-    const int max_epl = is_real ? 8 : 4;
+    // rows per thread: up to 4 (complex) / 8 (real) before the group widens to 16 warps
+    const int pref_epl = is_real ? 8 : 4;
     pl.G = 1;
-    while (pl.G < kConsumerWarps && int64_t(32) * pl.G * max_epl < m) pl.G <<= 1;
+    while (pl.G < kConsumerWarps && int64_t(32) * pl.G * pref_epl < m) pl.G <<= 1;
     int64_t epl = (m + 32 * pl.G - 1) / (32 * pl.G);
     pl.EPL = epl <= 1 ? 1 : epl <= 2 ? 2 : epl <= 4 ? 4 : 8;
-    require(int64_t(32) * pl.G * pl.EPL >= m, MNB_ERR_UNSUPPORTED, "pcg pass: m too large for one CTA");
+    require(int64_t(32) * pl.G * pl.EPL >= m, MNB_ERR_UNSUPPORTED,
+            "pcg pass: m = " + std::to_string(m) + " exceeds one CTA's rows (max " +
+                std::to_string(32 * kConsumerWarps * 8) + ")");
+    const int K = is_real ? (pl.EPL == 1 ? batch_cols<double, 1>() : pl.EPL == 2 ? batch_cols<double, 2>()
+                             : pl.EPL == 4 ? batch_cols<double, 4>() : batch_cols<double, 8>())
+                          : (pl.EPL == 1 ? batch_cols<double2, 1>() : pl.EPL == 2 ? batch_cols<double2, 2>()
+                             : pl.EPL == 4 ? batch_cols<double2, 4>() : batch_cols<double2, 8>());
     const int NG = kConsumerWarps / pl.G;
+    pl.K = K;
+    pl.stage_cols = int64_t(NG) * K;  // one batch per group per stage
     const int64_t col_bytes = m * esz;
-    // stage ~32 KiB, at least one column per group
-    int64_t cpg = std::max<int64_t>(1, (32 * 1024) / (NG * col_bytes));
-    pl.cols_per_group = int(cpg);
-    pl.stage_cols = NG * cpg;
-    pl.stages = 6;
     auto fits = [&](int stages) {
-        const SmemLayout L = smem_layout(m, pl.stage_cols, esz, stages);
+        const SmemLayout L = smem_layout(m, pl.stage_cols, esz, stages, 2 * K);
         const size_t epi = size_t(NG) * size_t(m) * 16 + size_t(NG) * 3 * 8;
         return std::max(L.total, epi + 64) <= size_t(220 * 1024);
     };
+    // ~192 KiB of stages in flight per SM (the ring is released as soon as a stage is in registers)
+    pl.stages = int(std::max<int64_t>(2, std::min<int64_t>(8, (192 * 1024) / std::max<int64_t>(1, pl.stage_cols * col_bytes))));
     while (pl.stages > 2 && !fits(pl.stages)) --pl.stages;
     require(fits(pl.stages), MNB_ERR_UNSUPPORTED, "pcg pass: stage does not fit in shared memory");
-    const SmemLayout L = smem_layout(m, pl.stage_cols, esz, pl.stages);
+    const SmemLayout L = smem_layout(m, pl.stage_cols, esz, pl.stages, 2 * K);
     const size_t epi = size_t(NG) * size_t(m) * 16 + size_t(NG) * 3 * 8;
     pl.smem = std::max(L.total, epi + 64);
     const int64_t max_grid = (n + pl.stage_cols - 1) / pl.stage_cols;
     pl.grid = int(std::max<int64_t>(1, std::min<int64_t>(num_sms, max_grid)));
+    // contiguous columns per CTA; even so that a real A with odd m stays 16-byte aligned for TMA
+    pl.per_cta = (n + pl.grid - 1) / pl.grid;
+    pl.per_cta += pl.per_cta & 1;
+    pl.grid = int(std::max<int64_t>(1, (n + pl.per_cta - 1) / pl.per_cta));
     return pl;
 }
 

@@ -47,8 +47,9 @@ struct PcgPassArgs {
 
 struct PcgPlan {
     int grid = 0;
-    int G = 1, EPL = 1, cols_per_group = 1, stages = 4;
-    int64_t stage_cols = 1;
+    int G = 1, EPL = 1, K = 1, stages = 4;  // warps per group, rows per thread, columns per batch
+    int64_t stage_cols = 1;                  // columns per shared-memory stage (groups x K)
+    int64_t per_cta = 1;                     // contiguous columns per CTA
     size_t smem = 0;
 };
 PcgPlan plan_pcg_pass(int64_t m, int64_t n, int is_real, int num_sms);

@@ -151,20 +151,23 @@ __host__ __device__ constexpr int log2c() { return V <= 1 ? 0 : 1 + log2c<V / 2>
 // 32 G); NG = 16/G groups split each shared-memory stage, K columns each.
 // Per batch of K columns a warp forms K partial dot products, reduces them
 // in-warp (xreduce), publishes them to shared memory, and -- one named
-// barrier later -- sums the G warp partials into t.  The loop is software
-// pipelined: the dot products of batch b+1 are issued between the barrier
-// and the axpy of batch b, so the reduction latency hides behind FMA work,
-// and a stage is handed back to the TMA producer as soon as it sits in
-// registers.  All sums run in a fixed order (bitwise reproducible).
-template <typename AT, int EPL>
-__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int G, int stages, int64_t C,
+// barrier later -- sums the G warp partials into t, then does the axpy.
+// A stage is handed back to the TMA producer (thread 0) as soon as it sits
+// in registers.  All sums run in a fixed order (bitwise reproducible).
+//
+// GT != 0: compile-time group width with m == 32*GT*EPL exactly (every
+// BASELINE shape), so shared-memory offsets are immediates and no row is
+// masked; GT == 0 is the generic kernel (runtime G, masked rows).
+template <typename AT, int EPL, int GT>
+__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int g_rt, int stages, int64_t C,
                                                                int64_t per) {
     constexpr int K = batch_cols<AT, EPL>();
     constexpr int V = 2 * K;
     extern __shared__ __align__(128) unsigned char smem[];
     if (p.state && p.state->done) return;  // uniform: converged loops cost one launch
-    const int64_t m = p.m;
-    const int mi = int(m);
+    const int G = GT ? GT : g_rt;
+    const int mi = GT ? 32 * GT * EPL : int(p.m);
+    const int64_t m = mi;
     constexpr int esz = int(sizeof(AT));
     const SmemLayout L = smem_layout(m, C, esz, stages, V);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -174,10 +177,11 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     const int NG = kConsumerWarps / G;
     const int64_t cb = min(p.n, int64_t(blockIdx.x) * per), ce = min(p.n, cb + per);
     const int64_t nstage = (ce - cb + C - 1) / C;
-    const bool init = p.mode == PCG_INIT;
-    const bool need_t = init || p.mode == PCG_CG;
-    const bool need_r = p.mode == PCG_CG;
-    const double alpha_prev = (p.mode == PCG_CG && p.state) ? p.state->alpha : 0.0;
+    const int mode = p.mode;
+    const bool init = mode == PCG_INIT;
+    const bool need_t = init || mode == PCG_CG;
+    const bool need_r = mode == PCG_CG;
+    const double alpha_prev = (mode == PCG_CG && p.state) ? p.state->alpha : 0.0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -188,12 +192,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     }
     __syncthreads();
 
-    // Producer (thread 0): fill stage s into slot s % stages.  The first
-    // `stages` fills are issued here; later ones from the consumer loop once
-    // every warp has moved the previous occupant of the slot into registers.
-    auto produce = [&](int64_t s) {
-        const int slot = int(s % stages);
-        if (s >= stages) mbar_wait(&empty[slot], uint32_t(((s / stages) - 1) & 1));
+    // Producer (thread 0): fill stage s into `slot`.  The first `stages`
+    // fills are issued here; later ones from the consumer loop, each after
+    // every warp has moved the slot's previous occupant into registers.
+    auto produce = [&](int64_t s, int slot) {
         const int64_t c0 = cb + s * C;
         const int64_t cc = min(C, ce - c0);
         unsigned char* st = smem + slot * L.stage_bytes;
@@ -209,13 +211,14 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
         if (need_r) bulk_g2s(st + L.tileR, p.r + c0, vbytes, &full[slot]);
     };
     if (threadIdx.x == 0)
-        for (int64_t s = 0; s < nstage && s < stages; ++s) produce(s);
+        for (int s = 0; s < nstage && s < stages; ++s) produce(s, s);
 
     // ---------------------------------------------------------- consumers
     const int gq = warp / G, wig = warp % G;
     const int row0 = wig * 32 + lane, rstep = 32 * G;
     double2 wreg[EPL], sacc[EPL];
 #define ROW(e) (row0 + (e) * rstep)
+#define ROW_OK(e) (GT != 0 || ROW(e) < mi)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
         sacc[e] = make_double2(0.0, 0.0);
@@ -227,40 +230,45 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
         if (!init) {
 #pragma unroll
             for (int e = 0; e < EPL; ++e)
-                if (ROW(e) < mi) wreg[e] = p.w[ROW(e)];
+                if (ROW_OK(e)) wreg[e] = p.w[ROW(e)];
         }
-        // lane k < K of the epilogue warp carries column k's t_old / r
-        AT a0[K][EPL];
-        double2 to0 = make_double2(0.0, 0.0), r0 = to0;
-        double2 tin0[K];  // INIT: t = c for all K columns (every lane)
-        double v0[V];
+        AT a[K][EPL];
+        double v[V];
+        int lslot = 0, pslot = 0, cslot = 0;  // consumer load slot, producer refill slot, current batch slot
+        uint32_t lph = 0, pph = 0;
+        int64_t c0 = cb;
 
-        auto load = [&](int64_t s, AT (&a)[K][EPL], double2& told, double2& rk, double2 (&tin)[K]) {
-            const int slot = int(s % stages);
-            mbar_wait(&full[slot], uint32_t((s / stages) & 1));
-            const int64_t cc = min(C, ce - (cb + s * C));
-            const unsigned char* st = smem + slot * L.stage_bytes;
-            const AT* tA = reinterpret_cast<const AT*>(st + L.tileA);
-            const double2* tT = reinterpret_cast<const double2*>(st + L.tileT);
-            const double2* tR = reinterpret_cast<const double2*>(st + L.tileR);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int col = gq * K + k;
-#pragma unroll
-                for (int e = 0; e < EPL; ++e)
-                    a[k][e] = (col < cc && ROW(e) < mi) ? tA[col * mi + ROW(e)] : zero_of<AT>();
-                if (init) tin[k] = col < cc ? tT[col] : make_double2(0.0, 0.0);
+        // The slot of batch s is released when batch s+1 is loaded, so the
+        // epilogue of batch s can still read its t_old / r / c from the stage.
+        auto load = [&](int64_t cc, bool release_prev) {
+            if (release_prev) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[cslot]);
             }
-            const int myc = gq * K + lane;
-            if (p.mode == PCG_CG && lane < K && myc < cc) {
-                told = tT[myc];
-                rk = tR[myc];
+            mbar_wait(&full[lslot], lph);
+            const unsigned char* st = smem + lslot * L.stage_bytes;
+            const AT* tA = reinterpret_cast<const AT*>(st + L.tileA) + gq * K * mi + row0;
+            if (cc == C) {  // uniform: every stage but possibly the last
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e) a[k][e] = ROW_OK(e) ? tA[k * mi + e * rstep] : zero_of<AT>();
+            } else {
+                const int have = int(cc) - gq * K;  // columns of this group present in the stage
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int e = 0; e < EPL; ++e)
+                        a[k][e] = (k < have && ROW_OK(e)) ? tA[k * mi + e * rstep] : zero_of<AT>();
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[slot]);
+            cslot = lslot;
+            if (++lslot == stages) {
+                lslot = 0;
+                lph ^= 1u;
+            }
         };
-        // partial dot products of one batch, reduced in-warp and published
-        auto dots = [&](const AT (&a)[K][EPL], double (&v)[V], int buf) {
+        // partial dot products of the batch, reduced in-warp and published
+        auto dots = [&](int buf) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 double2 part = make_double2(0.0, 0.0);
@@ -272,12 +280,17 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
             xreduce<V>(v, lane);
             if (G > 1 && (lane & ((32 / V) - 1)) == 0) red[(buf * G + wig) * V + (lane >> (5 - log2c<V>()))] = v[0];
         };
-        // t of one batch from the published partials
-        auto gather_t = [&](const double (&v)[V], int buf, double2 (&t)[K]) {
+        // t of the batch from the published partials (or from v when G == 1)
+        auto gather_t = [&](int buf, double2 (&t)[K]) {
             double acc;
             if (G > 1) {
-                acc = 0.0;
-                for (int j = lane; j < G * V; j += 32) acc += red[buf * G * V + j];
+                // G*V partials: lane L sums entries L, L+32, ... (all of value L % V)
+                const double* rb = red + buf * G * V;
+                acc = rb[lane < G * V ? lane : 0];
+                if (lane >= G * V) acc = 0.0;
+#pragma unroll
+                for (int j = 1; j < (16 * V) / 32; ++j)
+                    if (lane + 32 * j < G * V) acc += rb[lane + 32 * j];
 #pragma unroll
                 for (int mask = V; mask < 32; mask <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, mask);
 #pragma unroll
@@ -292,22 +305,38 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
                                         __shfl_sync(0xffffffffu, acc, (2 * k + 1) << sh));
             }
         };
-        // axpy + per-column epilogue of batch s
-        auto finish = [&](int64_t s, const AT (&a)[K][EPL], const double2 (&t)[K], double2 told, double2 rk) {
+
+        int64_t cc = min(C, ce - c0);
+        load(cc, false);
+        if (!init) dots(0);
+        for (int64_t s = 0; s < nstage; ++s) {
+            const int buf = int(s & 1);
+            if (G > 1 && !init) named_bar(1 + gq, G * 32);
+            const unsigned char* cst = smem + cslot * L.stage_bytes;
+            const double2* tT = reinterpret_cast<const double2*>(cst + L.tileT) + gq * K;
+            const double2* tR = reinterpret_cast<const double2*>(cst + L.tileR) + gq * K;
+            double2 t[K];
+            if (init) {
+                const int have = int(cc) - gq * K;
+#pragma unroll
+                for (int k = 0; k < K; ++k) t[k] = k < have ? tT[k] : make_double2(0.0, 0.0);
+            } else {
+                gather_t(buf, t);
+            }
 #pragma unroll
             for (int k = 0; k < K; ++k)
 #pragma unroll
                 for (int e = 0; e < EPL; ++e) axpy_acc<AT>(sacc[e], a[k][e], t[k]);
-            const int64_t c0 = cb + s * C;
-            const int64_t cc = min(C, ce - c0);
-            const int myc = gq * K + lane;
-            if (wig == 0 && lane < K && myc < cc) {
+            // per-column epilogue (lane k < K of the group's first warp owns column k)
+            if (wig == 0 && lane < K && gq * K + lane < cc) {
                 double2 tk = t[0];
 #pragma unroll
                 for (int k = 1; k < K; ++k)
                     if (lane == k) tk = t[k];
-                const int64_t col = c0 + myc;
-                if (p.mode == PCG_CG) {
+                const int64_t col = c0 + gq * K + lane;
+                if (mode == PCG_CG) {
+                    const double2 told = tT[lane];
+                    double2 rk = tR[lane];
                     rk.x = fma(-alpha_prev, told.x, rk.x);
                     rk.y = fma(-alpha_prev, told.y, rk.y);
                     rr = fma(rk.x, rk.x, fma(rk.y, rk.y, rr));
@@ -322,27 +351,19 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
                 }
                 qq = fma(tk.x, tk.x, fma(tk.y, tk.y, qq));
             }
-        };
-        // one step: finish batch s (already reduced and published), then load
-        // and publish batch s+1.  A single register batch keeps the kernel at
-        // <= 128 registers; 16 warps per SM cover the reduction latency.
-        load(0, a0, to0, r0, tin0);
-        if (!init) dots(a0, v0, 0);
-        for (int64_t s = 0; s < nstage; ++s) {
-            const int buf = int(s & 1);
-            if (G > 1 && !init) named_bar(1 + gq, G * 32);
-            double2 t[K];
-            if (init) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) t[k] = tin0[k];
-            } else {
-                gather_t(v0, buf, t);
-            }
-            finish(s, a0, t, to0, r0);
             if (s + 1 < nstage) {
-                load(s + 1, a0, to0, r0, tin0);
-                if (threadIdx.x == 0 && s + stages < nstage) produce(s + stages);
-                if (!init) dots(a0, v0, buf ^ 1);
+                c0 += C;
+                cc = min(C, ce - c0);
+                load(cc, true);
+                if (threadIdx.x == 0 && s + stages < nstage) {
+                    mbar_wait(&empty[pslot], pph);
+                    produce(s + stages, pslot);
+                    if (++pslot == stages) {
+                        pslot = 0;
+                        pph ^= 1u;
+                    }
+                }
+                if (!init) dots(buf ^ 1);
             }
         }
     }
@@ -351,25 +372,24 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     __syncthreads();  // all stages consumed: the stage ring is free
     double2* sred = reinterpret_cast<double2*>(smem);  // [NG][m]
     double* scal = reinterpret_cast<double*>(smem + size_t(NG) * size_t(m) * 16);
-    {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e)
-            if (ROW(e) < mi) sred[gq * mi + ROW(e)] = sacc[e];
-        if (wig == 0) {
-            // lanes >= K hold zeros; fixed-order butterfly
+    for (int e = 0; e < EPL; ++e)
+        if (ROW_OK(e)) sred[gq * mi + ROW(e)] = sacc[e];
+    if (wig == 0) {
+        // lanes >= K hold zeros; fixed-order butterfly
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                qq += __shfl_xor_sync(0xffffffffu, qq, o);
-                rt += __shfl_xor_sync(0xffffffffu, rt, o);
-                rr += __shfl_xor_sync(0xffffffffu, rr, o);
-            }
-            if (lane == 0) {
-                scal[gq * 3 + 0] = qq;
-                scal[gq * 3 + 1] = rt;
-                scal[gq * 3 + 2] = rr;
-            }
+        for (int o = 16; o > 0; o >>= 1) {
+            qq += __shfl_xor_sync(0xffffffffu, qq, o);
+            rt += __shfl_xor_sync(0xffffffffu, rt, o);
+            rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        }
+        if (lane == 0) {
+            scal[gq * 3 + 0] = qq;
+            scal[gq * 3 + 1] = rt;
+            scal[gq * 3 + 2] = rr;
         }
     }
+#undef ROW_OK
 #undef ROW
     __syncthreads();
     double2* ps = p.part_s + int64_t(blockIdx.x) * m;
@@ -630,12 +650,31 @@ __global__ void init_state_kernel(CgState* st, double tau, double dup, long long
     *st = z;
 }
 
-template <typename AT, int EPL>
+template <typename AT, int EPL, int GT>
 void launch_typed(const PcgPassArgs& a, const PcgPlan& pl, cudaStream_t stream) {
-    auto k = pcg_pass_kernel<AT, EPL>;
+    auto k = pcg_pass_kernel<AT, EPL, GT>;
     MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)));
     k<<<pl.grid, kThreads, pl.smem, stream>>>(a, pl.G, pl.stages, pl.stage_cols, pl.per_cta);
     MNB_LAUNCH_CHECK();
+}
+
+// Exact shapes m == 32*G*EPL get the compile-time-G kernel; the rest the generic one.
+template <typename AT, int EPL>
+void launch_epl(const PcgPassArgs& a, const PcgPlan& pl, cudaStream_t stream) {
+    const bool exact = a.m == int64_t(32) * pl.G * EPL;
+    if (exact) {
+        if constexpr (EPL == 4 || EPL == 8) {
+            switch (pl.G) {
+                case 2: return launch_typed<AT, EPL, 2>(a, pl, stream);
+                case 4: return launch_typed<AT, EPL, 4>(a, pl, stream);
+                case 8: return launch_typed<AT, EPL, 8>(a, pl, stream);
+                case 16: return launch_typed<AT, EPL, 16>(a, pl, stream);
+                default: break;
+            }
+        }
+        if (pl.G == 1) return launch_typed<AT, EPL, 1>(a, pl, stream);
+    }
+    launch_typed<AT, EPL, 0>(a, pl, stream);
 }
 
 }  // namespace
@@ -684,17 +723,17 @@ PcgPlan plan_pcg_pass(int64_t m, int64_t n, int is_real, int num_sms) {
 void launch_pcg_pass(const PcgPassArgs& a, const PcgPlan& pl, cudaStream_t stream) {
     if (a.is_real) {
         switch (pl.EPL) {
-            case 1: launch_typed<double, 1>(a, pl, stream); break;
-            case 2: launch_typed<double, 2>(a, pl, stream); break;
-            case 4: launch_typed<double, 4>(a, pl, stream); break;
-            default: launch_typed<double, 8>(a, pl, stream); break;
+            case 1: launch_epl<double, 1>(a, pl, stream); break;
+            case 2: launch_epl<double, 2>(a, pl, stream); break;
+            case 4: launch_epl<double, 4>(a, pl, stream); break;
+            default: launch_epl<double, 8>(a, pl, stream); break;
         }
     } else {
         switch (pl.EPL) {
-            case 1: launch_typed<double2, 1>(a, pl, stream); break;
-            case 2: launch_typed<double2, 2>(a, pl, stream); break;
-            case 4: launch_typed<double2, 4>(a, pl, stream); break;
-            default: launch_typed<double2, 8>(a, pl, stream); break;
+            case 1: launch_epl<double2, 1>(a, pl, stream); break;
+            case 2: launch_epl<double2, 2>(a, pl, stream); break;
+            case 4: launch_epl<double2, 4>(a, pl, stream); break;
+            default: launch_epl<double2, 8>(a, pl, stream); break;
         }
     }
 }

@@ -12,6 +12,8 @@
 // butterflies; passes exchange data through shared memory in place (all
 // reads, barrier, all writes).  Mixed-radix Stockham ordering, so the output
 // is in natural order with no bit reversal.  Radices 16, 8, 4, 3, 2.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -147,7 +149,7 @@ struct FftCta {
     __device__ __forceinline__ void gstore(int f, double2 v) const {
         if (!row_ok) return;
         if (a.mode == FFT_OUT_TWIDDLE) {
-            const int64_t e = (int64_t(f) * b) % a.n_total;
+            const int64_t e = int64_t(f) * b;  // f < n2, b < n1: already below n
             double2 w = c_mul(__ldg(a.tw4_hi + (e >> a.tw4_shift)), __ldg(a.tw4_lo + (e & ((int64_t(1) << a.tw4_shift) - 1))));
             if (INV) w.y = -w.y;
             v = c_mul(v, w);
@@ -209,7 +211,7 @@ struct FftCta {
 };
 
 template <int Rb, int E, bool INV>
-__global__ void __launch_bounds__(1024) fft_pass_kernel(const FftPassArgs a) {
+__global__ void __launch_bounds__(512) fft_pass_kernel(const FftPassArgs a) {
     extern __shared__ double2 sm[];
     FftCta<Rb, E, INV> cta{a, sm, int(threadIdx.x % Rb), int(threadIdx.x / Rb), a.N / E, 0, 0, false};
     cta.row = int64_t(blockIdx.x) * Rb + cta.r;
@@ -261,16 +263,32 @@ __global__ void dft_direct_kernel(const FftPassArgs a) {
 template <int Rb, int E>
 void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
     const int threads = Rb * a.N / E;
+    if (threads > 512) throw Error(MNB_ERR_INTERNAL, "fft: more than 512 threads per CTA");
     const size_t smem = size_t(Rb) * a.N * sizeof(double2);
     dim3 grid(ceil_div(a.rows, Rb), unsigned(a.batches));
-    if (a.inverse) {
-        auto k = fft_pass_kernel<Rb, E, true>;
-        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k<<<grid, threads, smem, stream>>>(a);
+    // Clusters of adjacent row blocks are co-scheduled, so the DRAM sees the
+    // neighbouring Rb*16-byte pieces of one index together (longer bursts).
+    int cl = 1;
+    if (const char* e = std::getenv("MNB_FFT_CLUSTER")) cl = std::max(1, std::atoi(e));
+    while (cl > 1 && grid.x % cl) cl >>= 1;
+    auto kern = a.inverse ? fft_pass_kernel<Rb, E, true> : fft_pass_kernel<Rb, E, false>;
+    MNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (cl > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MNB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
     } else {
-        auto k = fft_pass_kernel<Rb, E, false>;
-        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k<<<grid, threads, smem, stream>>>(a);
+        kern<<<grid, threads, smem, stream>>>(a);
     }
     MNB_LAUNCH_CHECK();
 }
@@ -328,6 +346,7 @@ void launch_fft_pass(const FftPassArgs& a, cudaStream_t stream) {
     }
     switch (a.Rb) {
         case 1: launch_rb<1>(a, stream); break;
+        case 2: launch_rb<2>(a, stream); break;
         case 4: launch_rb<4>(a, stream); break;
         case 8: launch_rb<8>(a, stream); break;
         default: throw Error(MNB_ERR_INTERNAL, "fft: unsupported rows per CTA");

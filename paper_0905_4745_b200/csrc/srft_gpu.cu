@@ -10,6 +10,7 @@
 //   FB  fft:    length-n1 DFTs over k1, keep sampled f = f2 + n2 f1, scale n^{-1/2} -> S
 // (n <= 2048: one FFT launch does the whole transform and the sampling.)
 #include <cmath>
+#include <cstdlib>
 
 #include "context.cuh"
 
@@ -43,7 +44,12 @@ void make_len_plan(FftLenPlan& p, int64_t N, cudaStream_t stream) {
     fill_twiddles(p.tw, N, N, 1, stream);
 }
 
-int rows_per_cta(int N) { return N <= 1024 ? 8 : 4; }
+int rows_per_cta(const FftLenPlan& p) {
+    int rb = p.N <= 1024 ? 8 : 4;
+    if (const char* e = std::getenv("MNB_FFT_RB")) rb = std::max(1, std::min(rb, std::atoi(e)));  // tuning knob
+    while (rb > 1 && rb * p.N / std::max(p.E, 1) > 512) rb >>= 1;
+    return rb;
+}
 
 FftPassArgs base_args(const FftLenPlan& p) {
     FftPassArgs a;
@@ -92,7 +98,7 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
               double* ms_a, double* ms_b) {
     FftPlan& P = ctx.fft_plan(n);
     const double scale = 1.0 / std::sqrt(double(n));
-    auto rb = [&](int N) { return rows == 1 ? 1 : rows_per_cta(N); };
+    auto rb = [&](const FftLenPlan& lp) { return rows == 1 ? 1 : rows_per_cta(lp); };
     if (P.single) {
         FftPassArgs a = base_args(P.A);
         a.in = in;
@@ -106,7 +112,7 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
         a.nb = 1;
         a.sel = sel;
         a.scale = scale;
-        a.Rb = rb(P.A.N);
+        a.Rb = rb(P.A);
         a.rows = rows;
         a.batches = 1;
         a.inverse = inverse;
@@ -130,7 +136,7 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
         a.tw4_lo = P.tw4_lo.as<double2>();
         a.tw4_shift = P.tw4_shift;
         a.n_total = n;
-        a.Rb = rb(P.A.N);
+        a.Rb = rb(P.A);
         a.rows = rows;
         a.batches = P.n1;
         a.inverse = inverse;
@@ -151,7 +157,7 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
         a.nb = P.n2;
         a.sel = sel;
         a.scale = scale;
-        a.Rb = rb(P.B.N);
+        a.Rb = rb(P.B);
         a.rows = rows;
         a.batches = P.n2;
         a.inverse = inverse;

@@ -350,6 +350,7 @@ def main():
             "solve": {"lsq_iterations": last.lsq_iterations, "lsq_converged": last.lsq_converged,
                       "residual_norm": last.residual_norm, "c_norm_ratio": last.c_norm_ratio,
                       "step_seconds": last.step_seconds, "param_seconds": last.extra["param_seconds"],
+                      "total_seconds_host": last.extra.get("total_seconds"),
                       "sketch_seconds": last.extra["sketch_seconds"], "qr_seconds": last.extra["qr_seconds"],
                       "pcg_seconds": last.extra["pcg_seconds"],
                       "redistribute_seconds": last.extra["redistribute_seconds"],

@@ -341,7 +341,7 @@ static int srft_vec_op(mnb_context* ctx, const mnb_srft* op, const void* in, voi
         const auto& h = op->host;
         const size_t n = size_t(h.n), l = size_t(h.l);
         const size_t nin = which == 2 ? l : n, nout = which == 1 ? l : n;
-        mnb::SrftDev dev;
+        mnb::SrftDev& dev = c.op_dev[2];
         mnb::upload_srft(c, h, dev);
         double2* din = static_cast<double2*>(c.vec_m[6].ensure(std::max(nin, n) * 16));
         double2* dout = static_cast<double2*>(c.vec_m[7].ensure(std::max(nout, n) * 16));
@@ -365,7 +365,7 @@ int mnb_srft_apply_to_columns(mnb_context* ctx, const mnb_srft* op, void* out, i
         MNB_CUDA(cudaSetDevice(c.device));
         mnb::require(c.A != nullptr || c.n_local == 0, MNB_ERR_INVALID_ARGUMENT, "no problem matrix set");
         mnb::require(op->host.n == c.n_global, MNB_ERR_INVALID_ARGUMENT, "apply_to_columns: matrix must have n rows");
-        mnb::SrftDev dev;
+        mnb::SrftDev& dev = c.op_dev[2];
         mnb::upload_srft(c, op->host, dev);
         const size_t bytes = size_t(op->host.l) * size_t(c.m) * 16;
         double2* S = out_location == MNB_DEVICE ? static_cast<double2*>(out)

@@ -76,6 +76,7 @@ struct SrftDev {
     DevBuf blob;
     DevBuf dups;
     int64_t ndups = 0;
+    DevBuf chain_rec[2];  // per-step chain records of the sketch H stages: [0] P1 (tilde half), [1] P2
     template <class T> const T* at(size_t off) const { return reinterpret_cast<const T*>(blob.as<unsigned char>() + off); }
 };
 
@@ -107,6 +108,7 @@ struct Context {
     DevBuf rhs, flag, out_c;
     int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
     PinnedBuf pin_params[2], pin_small;
+    SrftDev op_dev[3];  // device copies of the operators: [0] T, [1] T', [2] standalone SRFT calls (grow-only)
     std::vector<cudaEvent_t> events;
     std::vector<unsigned char> host_work;  // cuSOLVER host workspace (kept alive across async calls)
 

@@ -152,6 +152,11 @@ void SrftHost::derive() {
     int32_t* halo = at<int32_t>(off_halo);
     chain_halos(at<double>(off_cssn), n, ch, halo, halo + 2 * nc);
     chain_halos(at<double>(off_cssn_tilde), n, ch, halo + nc, halo + 3 * nc);
+    max_span = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t lo = c > 0 ? c * ch.chunk - 1 : 0;
+        max_span = std::max<int64_t>(max_span, std::max(halo[c], halo[nc + c]) - lo + 1);
+    }
     // selection map: frequency -> first output slot; duplicates listed.
     int32_t* sel = at<int32_t>(off_sel);
     std::fill(sel, sel + n, -1);

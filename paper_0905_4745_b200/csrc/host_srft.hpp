@@ -47,6 +47,7 @@ struct SrftHost {
     int64_t n = 0, l = 0;
     int sampling = 0;        // MNB_WITHOUT_REPLACEMENT / MNB_WITH_REPLACEMENT
     int64_t max_mult = 1;    // max multiplicity of `sample` (lsq.cpp:31-39)
+    int64_t max_span = 0;    // longest forward-chain scan of any chunk (chunk + halo + 1 steps)
     ChainChunks ch;
 
     // ---- blob layout (byte offsets) ----

@@ -12,6 +12,7 @@
 // butterflies; passes exchange data through shared memory in place (all
 // reads, barrier, all writes).  Mixed-radix Stockham ordering, so the output
 // is in natural order with no bit reversal.  Radices 16, 8, 4, 3, 2.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -116,6 +117,36 @@ __device__ __forceinline__ void dft16(double2* x) {
         for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = t[4 * k1 + k2];
 }
 
+// dft16 without the closing register transpose: output frequency q is left in
+// x[4*(q%4) + q/4] (callers index it at compile time, no register moves).
+template <bool INV>
+__device__ __forceinline__ void dft16_np(double2* x) {
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(x[n2], x[n2 + 4], x[n2 + 8], x[n2 + 12]);
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, r = 0.70710678118654752440;
+    const double sg = INV ? 1.0 : -1.0;
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+        for (int k1 = 1; k1 < 4; ++k1) {
+            const int e = n2 * k1;
+            double wc, ws;
+            switch (e) {
+                case 1: wc = c1; ws = s1; break;
+                case 2: wc = r; ws = r; break;
+                case 3: wc = s1; ws = c1; break;
+                case 4: wc = 0.0; ws = 1.0; break;
+                case 6: wc = -r; ws = r; break;
+                case 9: wc = -c1; ws = -s1; break;
+                default: wc = 1.0; ws = 0.0; break;
+            }
+            x[n2 + 4 * k1] = c_mul(x[n2 + 4 * k1], make_double2(wc, sg * ws));
+        }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(x[4 * k1], x[4 * k1 + 1], x[4 * k1 + 2], x[4 * k1 + 3]);
+}
+__host__ __device__ constexpr int d16(int q) { return 4 * (q % 4) + q / 4; }
+
 template <int R, bool INV>
 __device__ __forceinline__ void dft_r(double2* x) {
     if constexpr (R == 2) dft2<INV>(x[0], x[1]);
@@ -131,6 +162,29 @@ __device__ __forceinline__ double2 tw_at(const double2* __restrict__ tw, int64_t
     return w;
 }
 
+__device__ __forceinline__ uint32_t sm_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tile_load(double2* dst, const double2* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sm_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(sm_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tile_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(sm_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
 // Load phase helper: first pass reads global, later passes read shared.
 template <int Rb, int E, bool INV>
 struct FftCta {
@@ -139,6 +193,10 @@ struct FftCta {
     int r, u, U;
     int64_t row, b;
     bool row_ok;
+    int64_t rbk = 0;                     // blocked mode: row block of this unit
+    uint64_t* bar = nullptr;             // blocked mode: tile mbarrier
+    const double2* next_tile = nullptr;  // blocked mode: tile to prefetch once the last pass has read smem
+    uint32_t tile_bytes = 0;
 
     __device__ __forceinline__ double2 gload(int idx) const {
         if (!row_ok) return make_double2(0.0, 0.0);
@@ -153,6 +211,10 @@ struct FftCta {
             double2 w = c_mul(__ldg(a.tw4_hi + (e >> a.tw4_shift)), __ldg(a.tw4_lo + (e & ((int64_t(1) << a.tw4_shift) - 1))));
             if (INV) w.y = -w.y;
             v = c_mul(v, w);
+            if (a.blocked) {  // [row block][f][b][Rb]: the next pass reads one contiguous tile
+                a.out[((rbk * a.N + f) * a.batches + b) * Rb + r] = v;
+                return;
+            }
             const int64_t col = int64_t(f) * a.out_fstride + b * a.out_bstride;
             a.out[(a.out_row0 + row) + col * a.ld_out] = v;
         } else if (a.mode == FFT_OUT_SELECT) {
@@ -193,6 +255,10 @@ struct FftCta {
             dft_r<R, INV>(&v[s * R]);
         }
         if (!first) __syncthreads();  // all in-place reads done before any write
+        if (last && next_tile && threadIdx.x == 0) {  // blocked mode: the tile buffer is free -> prefetch
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tile_load(sm, next_tile, tile_bytes, bar);
+        }
         // write
 #pragma unroll
         for (int s = 0; s < B; ++s) {
@@ -234,6 +300,282 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPassArgs a) {
     }
 }
 
+// Blocked four-step pass: unit (row block rbk of 8 rows, batch b) reads ONE
+// contiguous tile [N][8] (in + (rbk*batches + b)*N*8) with a TMA bulk copy,
+// so HBM sees 128 KiB sequential reads instead of N scattered 128-byte pieces.
+//
+// Persistent CTAs, N/2 threads (E = 16 elements each, the whole tile in
+// registers).  Shared memory = the tile buffer + a half-tile exchange buffer:
+//   wait tile -> registers -> barrier -> prefetch the NEXT tile into the
+//   buffer (TMA, overlapping every radix pass and the global stores of this
+//   unit) -> radix passes in registers; between passes the data is exchanged
+//   through the half buffer one 4-row half at a time (rows are independent
+//   transforms) -> the last pass stores to global (twiddled, blocked for the
+//   next pass, or the sampled frequencies).
+template <int E, bool INV>
+struct FftTile {
+    static constexpr int Rb = 8;
+    const FftPassArgs& a;
+    FftCta<Rb, E, INV>& cta;  // epilogue (gstore) and twiddle table
+    const int N, U, r, u;
+
+    // inputs of a radix-R pass: v[s*R + q] = x[u + s*U + q*N/R]
+    template <int R, class Src>
+    __device__ __forceinline__ void load(double2 (&v)[E], Src src) const {
+        constexpr int B = E / R;
+        const int NR = N / R;
+#pragma unroll
+        for (int s = 0; s < B; ++s)
+#pragma unroll
+            for (int q = 0; q < R; ++q) v[s * R + q] = src(u + s * U + q * NR);
+    }
+    template <int R>
+    __device__ __forceinline__ void compute(double2 (&v)[E], int Ns) const {
+        constexpr int B = E / R;
+        const int stride = N / (Ns * R);
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+            const int j = u + s * U;
+            const int k = j % Ns;
+            if (k != 0) {
+#pragma unroll
+                for (int q = 1; q < R; ++q) v[s * R + q] = c_mul(v[s * R + q], tw_at(a.tw, int64_t(k) * q * stride, INV));
+            }
+            dft_r<R, INV>(&v[s * R]);
+        }
+    }
+    // outputs of a radix-R pass: y[(j/Ns)*Ns*R + j%Ns + q*Ns] = v[s*R + q]
+    template <int R, class Dst>
+    __device__ __forceinline__ void store(const double2 (&v)[E], int Ns, Dst dst) const {
+        constexpr int B = E / R;
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+            const int j = u + s * U;
+            const int k = j % Ns;
+            const int idxD = (j / Ns) * Ns * R + k;
+#pragma unroll
+            for (int q = 0; q < R; ++q) dst(idxD + q * Ns, v[s * R + q]);
+        }
+    }
+};
+
+template <int E, bool INV>
+__global__ void __launch_bounds__(512, 1) fft_tile_kernel(const FftPassArgs a) {
+    constexpr int Rb = 8;
+    extern __shared__ double2 sm[];
+    const int N = a.N;
+    double2* T = sm;                          // tile [N][8]
+    double2* X = sm + size_t(N) * Rb;         // exchange [N][4]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(X + size_t(N) * 4);
+    const int r = int(threadIdx.x % Rb), u = int(threadIdx.x / Rb), U = N / E;
+    FftCta<Rb, E, INV> cta{a, sm, r, u, U, 0, 0, false};
+    const FftTile<E, INV> ft{a, cta, N, U, r, u};
+    const int64_t nrbk = (a.rows + Rb - 1) / Rb;
+    const int64_t units = nrbk * a.batches;
+    const int64_t tile = int64_t(N) * Rb;
+    const uint32_t tile_bytes = uint32_t(tile * 16);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int64_t unit = blockIdx.x;
+    if (threadIdx.x == 0 && unit < units) tile_load(T, a.in + unit * tile, tile_bytes, bar);
+    uint32_t phase = 0;
+    double2 v[E];
+    const int half = r >> 2, r4 = r & 3;
+    for (; unit < units; unit += gridDim.x) {
+        cta.rbk = unit / a.batches;
+        cta.b = unit - cta.rbk * a.batches;
+        cta.row = cta.rbk * Rb + r;
+        cta.row_ok = cta.row < a.rows;
+        tile_wait(bar, phase);
+        phase ^= 1u;
+        auto from_tile = [&](int idx) { return T[idx * Rb + r]; };
+        switch (a.radix[0]) {
+            case 16: if constexpr (E % 16 == 0) ft.template load<16>(v, from_tile); break;
+            case 8: if constexpr (E % 8 == 0) ft.template load<8>(v, from_tile); break;
+            case 4: if constexpr (E % 4 == 0) ft.template load<4>(v, from_tile); break;
+            case 3: if constexpr (E % 3 == 0) ft.template load<3>(v, from_tile); break;
+            default: if constexpr (E % 2 == 0) ft.template load<2>(v, from_tile); break;
+        }
+        __syncthreads();  // the tile buffer is free: fetch the next unit's tile behind the compute
+        const int64_t next = unit + gridDim.x;
+        if (threadIdx.x == 0 && next < units) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tile_load(T, a.in + next * tile, tile_bytes, bar);
+        }
+        int Ns = 1;
+        for (int p = 0; p < a.nradix; ++p) {
+            const int R = a.radix[p];
+            const bool last = p == a.nradix - 1;
+            auto to_global = [&](int o, double2 val) { cta.gstore(o, val); };
+            auto to_x = [&](int o, double2 val) { X[o * 4 + r4] = val; };
+            auto from_x = [&](int idx) { return X[idx * 4 + r4]; };
+#define MNB_TILE_STEP(RR)                                                          \
+    if constexpr (E % RR == 0) {                                                   \
+        ft.template compute<RR>(v, Ns);                                            \
+        if (last) {                                                                \
+            ft.template store<RR>(v, Ns, to_global);                               \
+        } else {                                                                   \
+            for (int h = 0; h < 2; ++h) {                                          \
+                if (half == h) ft.template store<RR>(v, Ns, to_x);                 \
+                __syncthreads();                                                   \
+                if (half == h) {                                                   \
+                    switch (a.radix[p + 1]) {                                      \
+                        case 16: if constexpr (E % 16 == 0) ft.template load<16>(v, from_x); break; \
+                        case 8: if constexpr (E % 8 == 0) ft.template load<8>(v, from_x); break;    \
+                        case 4: if constexpr (E % 4 == 0) ft.template load<4>(v, from_x); break;    \
+                        case 3: if constexpr (E % 3 == 0) ft.template load<3>(v, from_x); break;    \
+                        default: if constexpr (E % 2 == 0) ft.template load<2>(v, from_x); break;   \
+                    }                                                              \
+                }                                                                  \
+                __syncthreads();                                                   \
+            }                                                                      \
+        }                                                                          \
+    }
+            switch (R) {
+                case 16: MNB_TILE_STEP(16) break;
+                case 8: MNB_TILE_STEP(8) break;
+                case 4: MNB_TILE_STEP(4) break;
+                case 3: MNB_TILE_STEP(3) break;
+                default: MNB_TILE_STEP(2) break;
+            }
+#undef MNB_TILE_STEP
+            Ns *= R;
+        }
+    }
+}
+
+// Specialised N = 1024 blocked pass (radix 16 x 16 x 4, forward): the
+// structure of fft_tile_kernel with every stride a compile-time constant, the
+// length-1024 twiddles in shared memory, and the epilogue data of the unit
+// (four-step twiddles w_n^{f b}, or the frequency -> sample-slot map) gathered
+// into shared memory while pass 1 computes, so no global load sits on the
+// store path.  512 threads: row r = tid & 7, u = tid >> 3 (64 threads per row,
+// 16 elements each).
+template <bool SELECT>
+__global__ void __launch_bounds__(512, 1) fft1024_tile_kernel(const FftPassArgs a) {
+    constexpr int Rb = 8, N = 1024;
+    extern __shared__ double2 sm[];
+    double2* T = sm;             // tile [1024][8]   128 KiB
+    double2* X = T + N * Rb;     // exchange [1024][4]  64 KiB
+    double2* W = X + N * 4;      // w_1024^k           16 KiB
+    double2* Z = W + N;          // epilogue data of the unit (16 KiB)
+    int* Zs = reinterpret_cast<int*>(Z);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Z + N);
+    const int r = int(threadIdx.x & 7), u = int(threadIdx.x >> 3);
+    const int half = r >> 2, r4 = r & 3;
+    const int64_t nrbk = (a.rows + Rb - 1) / Rb;
+    const int64_t units = nrbk * a.batches;
+    constexpr int64_t tile = int64_t(N) * Rb;
+    constexpr uint32_t tile_bytes = uint32_t(tile * 16);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = __ldg(a.tw + i);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int64_t unit = blockIdx.x;
+    if (threadIdx.x == 0 && unit < units) tile_load(T, a.in + unit * tile, tile_bytes, bar);
+    uint32_t phase = 0;
+    const int64_t lo_mask = (int64_t(1) << a.tw4_shift) - 1;
+#define XI(o) (((o) << 2) + r4)
+    double2 v[16];
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t rbk = unit / a.batches, b = unit - rbk * a.batches;
+        const int64_t row = rbk * Rb + r;
+        // epilogue data for frequencies f = tid, tid + 512 (loads in flight during the tile wait and pass 1)
+        double2 zt[2];
+        int zs[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int64_t f = threadIdx.x + 512 * i;
+            if constexpr (SELECT) {
+                zs[i] = __ldg(a.sel + b + a.nb * f);
+            } else {
+                const int64_t e = f * b;  // < n
+                zt[i] = c_mul(__ldg(a.tw4_hi + (e >> a.tw4_shift)), __ldg(a.tw4_lo + (e & lo_mask)));
+            }
+        }
+        tile_wait(bar, phase);
+        phase ^= 1u;
+        // pass 1 (radix 16, Ns = 1): x[u + 64 q]
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = T[(u + 64 * q) * Rb + r];
+        __syncthreads();  // tile buffer free (and the previous unit's epilogue done with Z)
+        {
+            const int64_t next = unit + gridDim.x;
+            if (threadIdx.x == 0 && next < units) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tile_load(T, a.in + next * tile, tile_bytes, bar);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            if constexpr (SELECT) Zs[threadIdx.x + 512 * i] = zs[i];
+            else Z[threadIdx.x + 512 * i] = zt[i];
+        }
+        dft16_np<false>(v);
+        // -> y[16 u + q];   pass 2 (radix 16, Ns = 16) reads x[u + 64 q], twiddle w^{4 (u%16) q}
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (half == h) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) X[XI(16 * u + q)] = v[d16(q)];
+            }
+            __syncthreads();
+            if (half == h) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = X[XI(u + 64 * q)];
+            }
+            __syncthreads();
+        }
+        {
+            const int k = u & 15;
+#pragma unroll
+            for (int q = 1; q < 16; ++q) v[q] = c_mul(v[q], W[4 * k * q]);
+        }
+        dft16_np<false>(v);
+        // -> y[(u/16)*256 + u%16 + 16 q];   pass 3 (radix 4, Ns = 256) reads x[j + 256 q], j = u + 64 s
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (half == h) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) X[XI((u >> 4) * 256 + (u & 15) + 16 * q)] = v[d16(q)];
+            }
+            __syncthreads();
+            if (half == h) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[4 * s + q] = X[XI(u + 64 * s + 256 * q)];
+            }
+            __syncthreads();
+        }
+        const bool row_ok = row < a.rows;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int j = u + 64 * s;
+#pragma unroll
+            for (int q = 1; q < 4; ++q) v[4 * s + q] = c_mul(v[4 * s + q], W[j * q]);
+            dft4<false>(v[4 * s], v[4 * s + 1], v[4 * s + 2], v[4 * s + 3]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int f = j + 256 * q;
+                if constexpr (SELECT) {
+                    const int slot = Zs[f];
+                    if (slot >= 0 && row_ok) a.out[int64_t(slot) + (a.out_row0 + row) * a.ld_out] = c_scale(v[4 * s + q], a.scale);
+                } else {
+                    // blocked [row block][f][b][8] for pass B
+                    a.out[((rbk * N + f) * a.batches + b) * Rb + r] = c_mul(v[4 * s + q], Z[f]);
+                }
+            }
+        }
+    }
+#undef XI
+}
+
 // N == 1: the transform is the identity; only the epilogue (twiddle/select) runs.
 template <bool INV>
 __global__ void fft_len1_kernel(const FftPassArgs a) {
@@ -265,6 +607,35 @@ void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
     const int threads = Rb * a.N / E;
     if (threads > 512) throw Error(MNB_ERR_INTERNAL, "fft: more than 512 threads per CTA");
     const size_t smem = size_t(Rb) * a.N * sizeof(double2);
+    if (a.blocked) {
+        if constexpr (Rb == 8 && E == 16) {
+            if (a.N == 1024 && !a.inverse && a.nradix == 3 && a.radix[0] == 16 && a.radix[1] == 16 && a.radix[2] == 4) {
+                const size_t sm1024 = size_t(1024) * (8 + 4 + 1 + 1) * sizeof(double2) + 16;
+                auto kern = a.mode == FFT_OUT_SELECT ? fft1024_tile_kernel<true> : fft1024_tile_kernel<false>;
+                MNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1024)));
+                const int64_t units = int64_t(ceil_div(a.rows, Rb)) * a.batches;
+                const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, a.num_sms)));
+                kern<<<grid, 512, sm1024, stream>>>(a);
+                MNB_LAUNCH_CHECK();
+                return;
+            }
+        }
+        if constexpr (Rb == 8) {
+            auto kern = a.inverse ? fft_tile_kernel<E, true> : fft_tile_kernel<E, false>;
+            const size_t sm_total = size_t(a.N) * 12 * sizeof(double2) + 16;  // tile + half exchange + barrier
+            MNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_total)));
+            const int64_t units = int64_t(ceil_div(a.rows, Rb)) * a.batches;
+            // several CTAs per SM for short transforms (registers: <= 128 per thread)
+            const int per_sm = int(std::max<size_t>(1, std::min<size_t>({(228 * 1024) / (sm_total + 1024),
+                                                                        size_t(2048 / threads),
+                                                                        size_t(65536 / (threads * 128))})));
+            const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(a.num_sms) * per_sm)));
+            kern<<<grid, threads, sm_total, stream>>>(a);
+            MNB_LAUNCH_CHECK();
+            return;
+        }
+        throw Error(MNB_ERR_INTERNAL, "fft: blocked passes use 8-row tiles");
+    }
     dim3 grid(ceil_div(a.rows, Rb), unsigned(a.batches));
     // Clusters of adjacent row blocks are co-scheduled, so the DRAM sees the
     // neighbouring Rb*16-byte pieces of one index together (longer bursts).

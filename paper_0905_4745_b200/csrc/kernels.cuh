@@ -27,6 +27,29 @@ struct HStageArgs {
 };
 void launch_hstage(const HStageArgs& a, cudaStream_t stream);
 
+// Sketch H stage (forward chain over row blocks, cp.async ring; k_hchain.cu).
+struct HChainArgs {
+    const void* in = nullptr;          // element (r, k) = in[in_row0 + r + k*ld_in]
+    int in_real = 0, in_conj = 0;
+    int64_t ld_in = 0, in_row0 = 0;
+    const int32_t* gather = nullptr;   // step j reads column gather[j]
+    const double2* params = nullptr;   // [n][3] = {cs_j, zin_j, zout_{j+1}} (build_chain_params)
+    int has_zin = 0, has_zout = 0;
+    double2 zout0 = {1.0, 0.0};        // output diagonal at index 0
+    const int32_t* halo = nullptr;     // per-chunk start index
+    double2* out = nullptr;
+    int64_t ld_out = 0, out_row0 = 0;
+    int64_t rows = 0, n = 0, chunk = 0, nchunks = 0, max_span = 0;
+    int* nonfinite = nullptr;
+    // blocked output for the four-step FFT (n = n1*n2): element (row, o) at
+    // out + (row/8)*n*8 + ((o % n1)*n2 + o / n1)*8 + row%8; 0 = [n][ld_out] layout
+    int64_t blk_n1 = 0, blk_n2 = 0;
+};
+void launch_hchain(const HChainArgs& a, int num_sms, cudaStream_t stream);
+bool hchain_fits(int64_t max_span, int is_real);
+void build_chain_params(const double2* cssn, const double2* zin, const int32_t* zin_index, const double2* zout,
+                        int64_t n, double2* rec, cudaStream_t stream);
+
 // ---------------------------------------------------------------- FFT
 enum FftOutMode { FFT_OUT_TWIDDLE = 0, FFT_OUT_SELECT = 1, FFT_OUT_NATURAL = 2 };
 
@@ -54,6 +77,10 @@ struct FftPassArgs {
     int64_t rows = 0;                         // rows in this block (masking)
     int64_t batches = 1;                      // grid.y
     int inverse = 0;
+    // blocked four-step layout (sketch): input tile of unit (rbk, b) at in + (rbk*batches + b)*N*Rb,
+    // TWIDDLE output at out + ((rbk*N + f)*batches + b)*Rb + r (rows padded to a multiple of Rb)
+    int blocked = 0;
+    int num_sms = 148;
 };
 void launch_fft_pass(const FftPassArgs& a, cudaStream_t stream);
 // O(N^2) fallback for lengths without a 2^a 3^b factorisation (N <= 4096).

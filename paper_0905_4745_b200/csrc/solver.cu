@@ -355,7 +355,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
 
     // ---- Step 1: S = T A^*
     double t0 = now_s();
-    SrftDev Td;
+    SrftDev& Td = ctx.op_dev[0];
     upload_srft(ctx, T, Td);
     int* nonfinite = dev<int>(ctx.flag, 1);
     MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx.stream));
@@ -423,7 +423,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     t0 = now_s();
     fut_Tp.get();
     rep.param_seconds = t_param_T + t_param_Tp;
-    SrftDev Tpd;
+    SrftDev& Tpd = ctx.op_dev[1];
     upload_srft(ctx, Tp, Tpd);
     sk_s = 0.0;
     qr_s = 0.0;
@@ -483,7 +483,7 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
     SrftHost Tp;
     build_srft_host(Tp, cfg.sketch_size, n, cfg.stream_seed, cfg.sampling,
                     [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); }, [](unsigned char*) {}, 0);
-    SrftDev Tpd;
+    SrftDev& Tpd = ctx.op_dev[1];
     upload_srft(ctx, Tp, Tpd);
     SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, nullptr, nullptr, nullptr, nullptr);
     if (int64_t bad = deficient_count(ctx, eq.S, cfg.sketch_size, m, n); bad > 0)

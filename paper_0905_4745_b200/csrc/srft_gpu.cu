@@ -44,6 +44,9 @@ void make_len_plan(FftLenPlan& p, int64_t N, cudaStream_t stream) {
     fill_twiddles(p.tw, N, N, 1, stream);
 }
 
+// a blocked tile pass keeps 8 rows x N (+ half exchange) in shared memory, <= 512 threads
+bool fft_tile_fits(int N, int E) { return size_t(N) * 12 * 16 + 16 <= size_t(227 * 1024) && 8 * N / E <= 512; }
+
 int rows_per_cta(const FftLenPlan& p) {
     int rb = p.N <= 1024 ? 8 : 4;
     if (const char* e = std::getenv("MNB_FFT_RB")) rb = std::max(1, std::min(rb, std::atoi(e)));  // tuning knob
@@ -166,6 +169,53 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
         t.stop();
     }
 }
+
+// Four-step DFT of `rows` rows held in the blocked layout of the sketch
+// (see HChainArgs::blk_n1): pass A (length n2, twiddled) -> tmp (blocked for
+// pass B), pass B (length n1) keeps the sampled frequencies -> out.
+void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, double2* tmp, double2* out,
+                      int64_t ld_out, int64_t out_row0, const int32_t* sel, double* ms_a, double* ms_b) {
+    FftPlan& P = ctx.fft_plan(n);
+    {
+        FftPassArgs a = base_args(P.A);
+        a.in = in;
+        a.out = tmp;
+        a.mode = FFT_OUT_TWIDDLE;
+        a.blocked = 1;
+        a.num_sms = ctx.num_sms;
+        a.tw4_hi = P.tw4_hi.as<double2>();
+        a.tw4_lo = P.tw4_lo.as<double2>();
+        a.tw4_shift = P.tw4_shift;
+        a.n_total = n;
+        a.Rb = 8;
+        a.rows = rows;
+        a.batches = P.n1;
+        EventTimer t(ctx, ms_a, 2);
+        launch_fft_pass(a, ctx.stream);
+        ctx.launches += 1;
+        t.stop();
+    }
+    {
+        FftPassArgs a = base_args(P.B);
+        a.in = tmp;
+        a.out = out;
+        a.ld_out = ld_out;
+        a.out_row0 = out_row0;
+        a.mode = FFT_OUT_SELECT;
+        a.blocked = 1;
+        a.num_sms = ctx.num_sms;
+        a.nb = P.n2;
+        a.sel = sel;
+        a.scale = 1.0 / std::sqrt(double(n));
+        a.Rb = 8;
+        a.rows = rows;
+        a.batches = P.n2;
+        EventTimer t(ctx, ms_b, 3);
+        launch_fft_pass(a, ctx.stream);
+        ctx.launches += 1;
+        t.stop();
+    }
+}
 }  // namespace
 
 FftPlan& Context::fft_plan(int64_t n) {
@@ -218,6 +268,14 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
         MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // op.dups is pageable
     }
     ctx.fft_plan(op.n);
+    // per-step records of the two sketch H stages (k_hchain.cu)
+    const int64_t n = op.n;
+    double2* rec1 = static_cast<double2*>(dev.chain_rec[0].ensure(size_t(n) * 48));
+    double2* rec2 = static_cast<double2*>(dev.chain_rec[1].ensure(size_t(n) * 48));
+    build_chain_params(dev.at<double2>(op.off_cssn_tilde), dev.at<double2>(op.off_zeta_tilde),
+                       dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
+    build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
+    ctx.launches += 2;
 }
 
 static HStageArgs chain_args(const SrftDev& op, bool tilde, bool adjoint) {
@@ -243,51 +301,113 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
     size_t free_b = 0, total_b = 0;
     MNB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t have = ctx.ws_x1.bytes + ctx.ws_x2.bytes + free_b;
-    const size_t budget = have > (size_t(3) << 30) ? have - (size_t(3) << 30) : have / 2;
+    // keep room for what the solve allocates after the first sketch: the second
+    // sketch E (l x m), R'^{-1} twice (m x m), the second operator, QR workspaces
+    const size_t mm = size_t(ctx.m), ll = size_t(h.l);
+    const size_t reserve = (size_t(2) << 30) + 24 * ll * mm + 32 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
+    const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
     int64_t Ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
     if (Ms < rows) Ms = std::max<int64_t>(8, Ms & ~int64_t(7));
     Ms = std::max<int64_t>(1, std::min<int64_t>(Ms, rows));
-    double2* x1 = static_cast<double2*>(ctx.ws_x1.ensure(size_t(Ms) * size_t(n) * 16));
-    double2* x2 = static_cast<double2*>(ctx.ws_x2.ensure(size_t(Ms) * size_t(n) * 16));
+    const int64_t Mp = (Ms + 7) & ~int64_t(7);  // blocked layouts pad the slab to whole 8-row blocks
+    double2* x1 = static_cast<double2*>(ctx.ws_x1.ensure(size_t(Mp) * size_t(n) * 16));
+    double2* x2 = static_cast<double2*>(ctx.ws_x2.ensure(size_t(Mp) * size_t(n) * 16));
+    const FftPlan& FP = ctx.fft_plan(n);
+    // Four-step FFT with both passes' tiles (8 rows x N) in shared memory: P2 writes x2 in
+    // the blocked layout pass A reads as contiguous tiles, pass A writes the one pass B reads.
+    const bool blocked = hchain_fits(h.max_span, is_real) && !FP.single && !FP.A.direct && !FP.B.direct &&
+                         fft_tile_fits(FP.A.N, FP.A.E) && fft_tile_fits(FP.B.N, FP.B.E);
     const double scale = 1.0 / std::sqrt(double(n));
 
     for (int64_t s0 = 0; s0 < rows; s0 += Ms) {
         const int64_t rs = std::min(Ms, rows - s0);
+        const bool chained = hchain_fits(h.max_span, is_real);
         {  // P1: Z~, Pi~, Theta~, Z   (src/srft.cpp:52-55)
-            HStageArgs a = chain_args(op, true, false);
-            a.in = Ablk;
-            a.in_real = is_real;
-            a.in_conj = 1;  // column of B = A^H is conj(row of A)
-            a.ld_in = lda;
-            a.in_row0 = row0 + s0;
-            a.nonfinite = ctx.nonfinite;
-            a.gather = op.at<int32_t>(h.off_perm_tilde);
-            a.in_diag = op.at<double2>(h.off_zeta_tilde);
-            a.out = x1;
-            a.ld_out = Ms;
-            a.out_diag = op.at<double2>(h.off_zeta);
-            a.rows = rs;
             EventTimer t(ctx, kernel_ms ? &kernel_ms[0] : nullptr, 0);
-            launch_hstage(a, ctx.stream);
+            if (chained) {
+                HChainArgs a;
+                a.in = Ablk;
+                a.in_real = is_real;
+                a.in_conj = 1;  // column of B = A^H is conj(row of A)
+                a.ld_in = lda;
+                a.in_row0 = row0 + s0;
+                a.gather = op.at<int32_t>(h.off_perm_tilde);
+                a.params = op.chain_rec[0].as<double2>();
+                a.has_zin = 1;
+                a.has_zout = 1;
+                a.zout0 = h.at<double2>(h.off_zeta)[0];
+                a.halo = op.at<int32_t>(h.off_halo) + h.ch.nchunks;  // forward chain of Theta~
+                a.out = x1;
+                a.ld_out = Ms;
+                a.rows = rs;
+                a.n = n;
+                a.chunk = h.ch.chunk;
+                a.nchunks = h.ch.nchunks;
+                a.max_span = h.max_span;
+                a.nonfinite = ctx.nonfinite;
+                launch_hchain(a, ctx.num_sms, ctx.stream);
+            } else {
+                HStageArgs a = chain_args(op, true, false);
+                a.in = Ablk;
+                a.in_real = is_real;
+                a.in_conj = 1;
+                a.ld_in = lda;
+                a.in_row0 = row0 + s0;
+                a.nonfinite = ctx.nonfinite;
+                a.gather = op.at<int32_t>(h.off_perm_tilde);
+                a.in_diag = op.at<double2>(h.off_zeta_tilde);
+                a.out = x1;
+                a.ld_out = Ms;
+                a.out_diag = op.at<double2>(h.off_zeta);
+                a.rows = rs;
+                launch_hstage(a, ctx.stream);
+            }
             ctx.launches += 1;
             t.stop();
         }
         {  // P2: Pi, Theta, then D (src/srft.cpp:56-57,128)
-            HStageArgs a = chain_args(op, false, false);
-            a.in = x1;
-            a.ld_in = Ms;
-            a.gather = op.at<int32_t>(h.off_perm);
-            a.out = x2;
-            a.ld_out = Ms;
-            a.out_diag = op.at<double2>(h.off_d);
-            a.rows = rs;
             EventTimer t(ctx, kernel_ms ? &kernel_ms[1] : nullptr, 1);
-            launch_hstage(a, ctx.stream);
+            if (chained) {
+                HChainArgs a;
+                a.in = x1;
+                a.ld_in = Ms;
+                a.gather = op.at<int32_t>(h.off_perm);
+                a.params = op.chain_rec[1].as<double2>();
+                a.has_zout = 1;
+                a.zout0 = h.at<double2>(h.off_d)[0];
+                a.halo = op.at<int32_t>(h.off_halo);  // forward chain of Theta
+                a.out = x2;
+                a.ld_out = Ms;
+                if (blocked) {
+                    a.blk_n1 = FP.n1;
+                    a.blk_n2 = FP.n2;
+                }
+                a.rows = rs;
+                a.n = n;
+                a.chunk = h.ch.chunk;
+                a.nchunks = h.ch.nchunks;
+                a.max_span = h.max_span;
+                launch_hchain(a, ctx.num_sms, ctx.stream);
+            } else {
+                HStageArgs a = chain_args(op, false, false);
+                a.in = x1;
+                a.ld_in = Ms;
+                a.gather = op.at<int32_t>(h.off_perm);
+                a.out = x2;
+                a.ld_out = Ms;
+                a.out_diag = op.at<double2>(h.off_d);
+                a.rows = rs;
+                launch_hstage(a, ctx.stream);
+            }
             ctx.launches += 1;
             t.stop();
         }
         // F and S (src/srft.cpp:129-131)
-        fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
+        if (blocked)
+            fft_rows_blocked(ctx, n, x2, rs, x1, out, ldo, out_row0 + s0, op.at<int32_t>(h.off_sel),
+                             kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
+        else
+                    fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
                  kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
         if (op.ndups) {
             launch_copy_dups(out, ldo, out_row0 + s0, rs, op.dups.as<int32_t>(), op.ndups, ctx.stream);

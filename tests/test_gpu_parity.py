@@ -59,7 +59,10 @@ def test_apply_and_adjoint_match_oracle(ctx, l, n, mode):
     assert rel(op.apply_adjoint(v, ctx), ref.apply_adjoint(v)) <= 1e-13
 
 
-@pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160)])
+# the large-n cases exercise the blocked four-step passes (n = 2^20: both passes
+# length 1024, the specialised kernel; 2^19: 512 x 1024; 3*2^20: 1536 x 2048)
+@pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160),
+                                   (8, 1 << 20, 64), (12, 1 << 19, 48), (5, 3 << 20, 40)])
 def test_sketch_matches_oracle(ctx, m, n, l):
     A, _ = make_instance(m, n, kappa=1e3, seed=m + n)
     seed = mn.derive_seed(42, 11)

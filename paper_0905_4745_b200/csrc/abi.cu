@@ -1,4 +1,5 @@
 // extern "C" boundary (include/minnorm_b200.h): status codes in, exceptions out.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -50,6 +51,7 @@ void init_context(mnb::Context& c, int device) {
     MNB_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
     MNB_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.own_stream = true;
+    if (const char* q = std::getenv("MNB_QR")) c.cholqr = std::string(q) != "householder";
     if (cublasCreate(&c.cublas) != CUBLAS_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cublasCreate failed");
     cublasSetStream(c.cublas, c.stream);
     if (cusolverDnCreate(&c.cusolver) != CUSOLVER_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cusolverDnCreate failed");

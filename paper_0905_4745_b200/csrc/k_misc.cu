@@ -1,4 +1,6 @@
 // Small glue kernels of the hot path.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -50,6 +52,47 @@ void launch_scatter_add_sample(const double2* v, int64_t l, const int32_t* sampl
     MNB_CUDA(cudaMemsetAsync(w, 0, size_t(n) * sizeof(double2), stream));
     if (with_replacement) scatter_add_serial_kernel<<<1, 1, 0, stream>>>(v, l, sample, w);
     else scatter_sample_kernel<<<ceil_div(l, 256), 256, 0, stream>>>(v, l, sample, w);
+    MNB_LAUNCH_CHECK();
+}
+
+__global__ void zero_lower_kernel(double2* A, int64_t m) {
+    const int64_t j = blockIdx.y;  // column
+    for (int64_t i = j + 1 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+        A[i + j * m] = make_double2(0.0, 0.0);
+}
+
+void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream) {
+    if (m <= 1) return;
+    dim3 grid(unsigned(std::min<int64_t>(16, ceil_div(m, 256))), unsigned(m));
+    zero_lower_kernel<<<grid, 256, 0, stream>>>(A, m);
+    MNB_LAUNCH_CHECK();
+}
+
+__global__ void max_offset_kernel(const double2* A, int64_t m, unsigned long long* out) {
+    __shared__ double ws[8];
+    double mx = 0.0;
+    const int64_t total = m * m;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e % m, j = e / m;
+        if (i > j) continue;
+        double2 a = A[e];
+        if (i == j) a.x -= 1.0;
+        mx = fmax(mx, fmax(fabs(a.x), fabs(a.y)));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) mx = fmax(mx, ws[w]);
+        if (mx != mx) mx = 1e300;  // NaN: treat as not orthonormal
+        atomicMax(out, __double_as_longlong(mx));  // non-negative doubles order like their bit patterns
+    }
+}
+
+void launch_max_offset_from_identity(const double2* A, int64_t m, double* out, cudaStream_t stream) {
+    MNB_CUDA(cudaMemsetAsync(out, 0, sizeof(double), stream));
+    const int blocks = int(std::min<int64_t>(592, ceil_div(m * m, 256)));
+    max_offset_kernel<<<blocks, 256, 0, stream>>>(A, m, reinterpret_cast<unsigned long long*>(out));
     MNB_LAUNCH_CHECK();
 }
 

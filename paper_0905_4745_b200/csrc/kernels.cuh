@@ -90,6 +90,10 @@ void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream);
 bool plan_radices(int N, int& E, int* radix, int& nradix);
 
 // ---------------------------------------------------------------- misc
+// zero the strictly lower triangle of an m x m column-major matrix
+void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream);
+// out[0] = max_{i<=j} |A_ij - delta_ij| over the upper triangle (deterministic)
+void launch_max_offset_from_identity(const double2* A, int64_t m, double* out, cudaStream_t stream);
 void launch_copy_dups(double2* S, int64_t ldS, int64_t row0, int64_t rows, const int32_t* dups, int64_t ndups,
                       cudaStream_t stream);
 void launch_scatter_add_sample(const double2* v, int64_t l, const int32_t* sample, int with_replacement,

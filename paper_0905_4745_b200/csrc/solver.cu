@@ -259,20 +259,110 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
 
 // ------------------------------------------------------------- helpers ----
 struct SketchQr {
-    double2* S;
-    double2* tau;
+    double2* S;         // the sketch (Householder path: overwritten by geqrf's reflectors and R)
+    double2* tau;       // Householder path only
+    const double2* R;   // m x m upper triangle, leading dimension ldR
+    int64_t ldR;
+    bool householder;
 };
 
-SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, double* kernel_ms,
+// CholeskyQR2 of the l x m sketch, R only (S is left intact):
+//   G = S^H S = R1^H R1,  Q1 = S R1^{-1},  Q1^H Q1 = R2^H R2,  R = R2 R1.
+// Two Gram passes on tensor-core ZHERK instead of Householder panels (~3x
+// fewer cycles at the BASELINE shapes).  R equals Householder's R up to a
+// unitary diagonal D (R_hh = D R), which leaves every downstream quantity
+// unchanged: z = Q R^{-H} b with Q = Q1 R2^{-1}, and CG on A^H R'^{-1} is invariant under
+// R' -> D R' (the iterates rotate, their norms do not).  Stable while
+// eps * cond(S)^2 < 1; returns false (caller falls back to Householder, as
+// the reference) when a Cholesky breaks down or Q1 = S R1^{-1} is not orthonormal
+// to 1e-3 (cond(S) above ~2e6).  On success ctx.qwork holds Q1 and ctx.R2 holds R2.
+bool cholqr2_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R) {
+    const auto* Sc = reinterpret_cast<const cuDoubleComplex*>(S);
+    double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
+    double2* Q = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
+    int* info = dev<int>(ctx.qr_info, 2);
+    std::vector<double> diag(size_t(2 * m));
+    int info_h = 0;
+    auto potrf = [&](double2* A) {
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXpotrf_bufferSize(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m,
+                                                   CUDA_C_64F, A, m, CUDA_C_64F, &dws, &hws),
+                       "potrf_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXpotrf(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m, CUDA_C_64F, A, m,
+                                        CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
+                       "potrf");
+        launch_zero_lower(A, m, ctx.stream);
+        ctx.launches += 1;
+        MNB_CUDA(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        MNB_CUDA(cudaMemcpy2DAsync(diag.data(), 16, A, size_t(m + 1) * 16, 16, size_t(m), cudaMemcpyDeviceToHost,
+                                   ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    };
+    const double one = 1.0, zero = 0.0;
+    const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0);
+    // pass 1
+    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one, Sc, int(l), &zero,
+                             reinterpret_cast<cuDoubleComplex*>(G), int(m)),
+                 "zherk");
+    potrf(G);
+    if (info_h != 0) return false;
+    double dmax = 0.0, dmin = 1e300;
+    for (int64_t j = 0; j < m; ++j) {
+        const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
+        dmax = std::max(dmax, a);
+        dmin = std::min(dmin, a);
+    }
+    if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
+    MNB_CUDA(cudaMemcpyAsync(Q, S, size_t(l) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    cublas_check(cublasZtrsm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             int(l), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(G), int(m),
+                             reinterpret_cast<cuDoubleComplex*>(Q), int(l)),
+                 "ztrsm");
+    // pass 2: R2 = chol(Q1^H Q1).  Q1 must be nearly orthonormal (|G2 - I| ~ eps cond(S)^2) for
+    // the product R2 R1 to be accurate; otherwise the sketch is too ill-conditioned for CholeskyQR2.
+    double2* R2 = dev<double2>(ctx.R2, size_t(m) * size_t(m));
+    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
+                             reinterpret_cast<const cuDoubleComplex*>(Q), int(l), &zero,
+                             reinterpret_cast<cuDoubleComplex*>(R2), int(m)),
+                 "zherk");
+    double* dev_max = dev<double>(ctx.scratch, 512);
+    launch_max_offset_from_identity(R2, m, dev_max, ctx.stream);
+    ctx.launches += 1;
+    double gmax = 0.0;
+    MNB_CUDA(cudaMemcpyAsync(&gmax, dev_max, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (!(gmax < 1e-3)) return false;
+    potrf(R2);
+    if (info_h != 0) return false;
+    // R = R2 R1 (R1 in G; both upper with zeroed lower parts)
+    MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             int(m), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(R2), int(m),
+                             reinterpret_cast<const cuDoubleComplex*>(R), int(m), reinterpret_cast<cuDoubleComplex*>(R),
+                             int(m)),
+                 "ztrmm");
+    return true;
+}
+
+SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, DevBuf& Rbuf, double* kernel_ms,
                        double* sketch_s, double* qr_s, double* redistribute_s) {
     const int64_t l = op.host->l, m = ctx.m;
     double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
     double2* tau = dev<double2>(taubuf, size_t(m));
+    double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
     cudaEvent_t e0 = ctx.event(12), e1 = ctx.event(13), e2 = ctx.event(14);
     MNB_CUDA(cudaEventRecord(e0, ctx.stream));
     sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
-    qr_in_place(ctx, S, l, m, tau);
+    SketchQr out{S, tau, R, m, false};
+    if (!(ctx.cholqr && cholqr2_r(ctx, S, l, m, R))) {
+        qr_in_place(ctx, S, l, m, tau);
+        out.R = S;
+        out.ldR = l;
+        out.householder = true;
+    }
     MNB_CUDA(cudaEventRecord(e2, ctx.stream));
     MNB_CUDA(cudaEventSynchronize(e2));
     float a = 0.f, b = 0.f;
@@ -280,7 +370,7 @@ SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& ta
     MNB_CUDA(cudaEventElapsedTime(&b, e1, e2));
     if (sketch_s) *sketch_s += a * 1e-3;
     if (qr_s) *qr_s += b * 1e-3;
-    return {S, tau};
+    return out;
 }
 
 unsigned char* pinned_alloc(PinnedBuf& pb, size_t bytes) { return static_cast<unsigned char*>(pb.ensure(bytes)); }
@@ -361,7 +451,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx.stream));
     ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
     double qr_s = 0.0, sk_s = 0.0;
-    SketchQr sq = sketch_and_qr(ctx, Td, ctx.sk_S, ctx.tau_S, rep.sketch_kernel_ms, &sk_s, &qr_s,
+    SketchQr sq = sketch_and_qr(ctx, Td, ctx.sk_S, ctx.tau_S, ctx.R_S, rep.sketch_kernel_ms, &sk_s, &qr_s,
                                 &rep.redistribute_seconds);
     ctx.nonfinite = nullptr;
     {
@@ -382,18 +472,19 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
 
     // ---- Step 2: z = Q [R^{-H} b; 0]  (src/solver.cpp:85-97)
     t0 = now_s();
-    if (int64_t bad = deficient_count(ctx, sq.S, l, m, l); bad > 0)
+    if (int64_t bad = deficient_count(ctx, sq.R, sq.ldR, m, l); bad > 0)
         throw Error(MNB_ERR_RANK_DEFICIENCY,
                     "sketch S = T A* lost rank (" + std::to_string(bad) +
                         " dependent columns); the problem matrix is rank deficient",
                     bad);
     double2* z = dev<double2>(ctx.rhs, size_t(l));
-    MNB_CUDA(cudaMemsetAsync(z, 0, size_t(l) * 16, ctx.stream));
-    MNB_CUDA(cudaMemcpyAsync(z, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-    cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
-                             reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l), reinterpret_cast<cuDoubleComplex*>(z), 1),
-                 "ztrsv");
-    {
+    const auto* Rc = reinterpret_cast<const cuDoubleComplex*>(sq.R);
+    if (sq.householder) {
+        MNB_CUDA(cudaMemsetAsync(z, 0, size_t(l) * 16, ctx.stream));
+        MNB_CUDA(cudaMemcpyAsync(z, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
+                                 int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(z), 1),
+                     "ztrsv");
         int lwork = 0;
         cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
                                                    reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
@@ -407,6 +498,23 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                                         reinterpret_cast<cuDoubleComplex*>(z), int(l), work, lwork,
                                         dev<int>(ctx.qr_info, 1)),
                        "unmqr");
+    } else {
+        // z = Q [R^{-H} b; 0] with Q = S R^{-1} = Q1 R2^{-1}:  z = Q1 (R2^{-1} (R^{-H} b))
+        double2* w = dev<double2>(ctx.vec_m[6], size_t(m));
+        MNB_CUDA(cudaMemcpyAsync(w, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
+                                 int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(w), 1),
+                     "ztrsv");
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
+                                 reinterpret_cast<const cuDoubleComplex*>(ctx.R2.p), int(m),
+                                 reinterpret_cast<cuDoubleComplex*>(w), 1),
+                     "ztrsv");
+        const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0), czero = make_cuDoubleComplex(0.0, 0.0);
+        cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &cone,
+                                 reinterpret_cast<const cuDoubleComplex*>(ctx.qwork.p), int(l),
+                                 reinterpret_cast<const cuDoubleComplex*>(w), 1, &czero,
+                                 reinterpret_cast<cuDoubleComplex*>(z), 1),
+                     "zgemv");
     }
     sync(ctx);
     rep.step_seconds[1] = now_s() - t0;
@@ -427,16 +535,16 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     upload_srft(ctx, Tp, Tpd);
     sk_s = 0.0;
     qr_s = 0.0;
-    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, rep.sketch_kernel_ms, &sk_s, &qr_s,
+    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, rep.sketch_kernel_ms, &sk_s, &qr_s,
                                 &rep.redistribute_seconds);
     rep.sketch_seconds[1] = sk_s;
     rep.qr_seconds[1] = qr_s;
-    if (int64_t bad = deficient_count(ctx, eq.S, l, m, n); bad > 0)
+    if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
         throw Error(MNB_ERR_RANK_DEFICIENCY,
                     "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
-    LsqResult ls = run_cg(ctx, c_loc, eq.S, l, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false);
+    LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false);
     rep.lsq_iterations = ls.iterations;
     rep.lsq_converged = ls.converged ? 1 : 0;
     rep.lsq_achieved_excess = ls.achieved_excess;
@@ -485,13 +593,13 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
                     [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); }, [](unsigned char*) {}, 0);
     SrftDev& Tpd = ctx.op_dev[1];
     upload_srft(ctx, Tp, Tpd);
-    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, nullptr, nullptr, nullptr, nullptr);
-    if (int64_t bad = deficient_count(ctx, eq.S, cfg.sketch_size, m, n); bad > 0)
+    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, nullptr, nullptr, nullptr, nullptr);
+    if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
         throw Error(MNB_ERR_RANK_DEFICIENCY,
                     "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
-    LsqResult ls = run_cg(ctx, c_dev, eq.S, cfg.sketch_size, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
+    LsqResult ls = run_cg(ctx, c_dev, eq.R, eq.ldR, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
                           residual_norms != nullptr);
     MNB_CUDA(cudaMemcpyAsync(y_host, y, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
     sync(ctx);

@@ -302,9 +302,9 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
     MNB_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const size_t have = ctx.ws_x1.bytes + ctx.ws_x2.bytes + free_b;
     // keep room for what the solve allocates after the first sketch: the second
-    // sketch E (l x m), R'^{-1} twice (m x m), the second operator, QR workspaces
+    // sketch E (l x m), the CholeskyQR2 copy (l x m), R, R', Gram, R'^{-1} twice (m x m), the second operator
     const size_t mm = size_t(ctx.m), ll = size_t(h.l);
-    const size_t reserve = (size_t(2) << 30) + 24 * ll * mm + 32 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
+    const size_t reserve = (size_t(2) << 30) + 40 * ll * mm + 96 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
     const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
     int64_t Ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
     if (Ms < rows) Ms = std::max<int64_t>(8, Ms & ~int64_t(7));

@@ -122,3 +122,24 @@ def test_solve_real_matrix(ctx):
     ref = O.solve_randomized(A, b, epsilon=1e-10)
     assert rel(rep.x, ref.x) <= 1e-9
     assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
+
+
+@pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (128, 8192, 1e8, 1e-10)])
+def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
+    """The sketch QRs run CholeskyQR2 (tensor-core ZHERK) when the sketch is
+    well enough conditioned and fall back to Householder (the reference's
+    HouseholderQR, src/solver.cpp:86, src/lsq.cpp:58) otherwise; both must give
+    the same solve."""
+    A, b = make_instance(m, n, kappa, seed=m + 3)
+    cfg = mn.SolverConfig(epsilon=eps, seed=42)
+    reps = {}
+    for mode in ("cholqr2", "householder"):
+        monkeypatch.setenv("MNB_QR", mode)
+        c = mn.Context(0)
+        reps[mode] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        c.close()
+    a, h = reps["cholqr2"], reps["householder"]
+    p = O.solve_classical(A, b)
+    assert rel(a.x, p) <= solve_tol(eps, kappa)
+    assert rel(a.x, h.x) <= solve_tol(eps, kappa)
+    assert abs(a.lsq_iterations - h.lsq_iterations) <= 1

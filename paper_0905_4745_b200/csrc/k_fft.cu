@@ -576,6 +576,92 @@ __global__ void __launch_bounds__(512, 1) fft1024_tile_kernel(const FftPassArgs 
 #undef XI
 }
 
+// Pass B of the sketch FFT with N = n1 = 1024, pruned to the sampled outputs.
+// Only ~l/n2 of the 1024 frequencies of a unit (row block rbk, f2 = b) are
+// kept (src/srft.cpp:131), so after the first radix-16 stage,
+//   Y_u[j] = sum_q x[u + 64 q] w_16^{j q}          (u < 64, j < 16),
+// each kept frequency f is a 64-term sum  X[f] = sum_u w_1024^{f u} Y_u[f mod 16]
+// taken by one warp (shuffle reduction) per (row, sample) pair.  The unit's
+// samples come from a CSR list (fb_off/fb_ent: per f2 the pairs (f1, slot)).
+// Shared-memory traffic and barriers drop to about a third of the full
+// 16x16x4 transform.
+__global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArgs a, const int32_t* __restrict__ off,
+                                                              const int32_t* __restrict__ ent) {
+    constexpr int Rb = 8, N = 1024;
+    extern __shared__ double2 sm[];
+    double2* T = sm;           // tile [1024][8]
+    double2* X = T + N * Rb;   // Y of one 4-row half: [16 j][64 u][4 r]
+    double2* W = X + N * 4;    // w_1024^k
+    uint64_t* bar = reinterpret_cast<uint64_t*>(W + N);
+    const int r = int(threadIdx.x & 7), u = int(threadIdx.x >> 3);
+    const int half = r >> 2, r4 = r & 3;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+    const int64_t nrbk = (a.rows + Rb - 1) / Rb;
+    const int64_t units = nrbk * a.batches;
+    constexpr int64_t tile = int64_t(N) * Rb;
+    constexpr uint32_t tile_bytes = uint32_t(tile * 16);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = __ldg(a.tw + i);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int64_t unit = blockIdx.x;
+    if (threadIdx.x == 0 && unit < units) tile_load(T, a.in + unit * tile, tile_bytes, bar);
+    uint32_t phase = 0;
+    double2 v[16];
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t rbk = unit / a.batches, b = unit - rbk * a.batches;
+        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        tile_wait(bar, phase);
+        phase ^= 1u;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = T[(u + 64 * q) * Rb + r];
+        __syncthreads();  // tile buffer free
+        {
+            const int64_t next = unit + gridDim.x;
+            if (threadIdx.x == 0 && next < units) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tile_load(T, a.in + next * tile, tile_bytes, bar);
+            }
+        }
+        if (cnt == 0) continue;  // uniform; the next iteration's barrier orders the tile reuse
+        dft16_np<false>(v);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+            if (half == h) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) X[(j * 64 + u) * 4 + r4] = v[d16(j)];
+            }
+            __syncthreads();
+            for (int p = warp; p < 4 * cnt; p += 16) {
+                const int rp = p & 3, s = p >> 2;
+                const int f = __ldg(ent + 2 * (e0 + s)), slot = __ldg(ent + 2 * (e0 + s) + 1);
+                const int j = f & 15;
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int uu = lane + 32 * t;
+                    const double2 y = X[(j * 64 + uu) * 4 + rp];
+                    const double2 w = W[(f * uu) & (N - 1)];
+                    acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
+                    acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                }
+                const int64_t row = rbk * Rb + h * 4 + rp;
+                if (lane == 0 && row < a.rows)
+                    a.out[int64_t(slot) + (a.out_row0 + row) * a.ld_out] = c_scale(acc, a.scale);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+
 // N == 1: the transform is the identity; only the epilogue (twiddle/select) runs.
 template <bool INV>
 __global__ void fft_len1_kernel(const FftPassArgs a) {
@@ -680,6 +766,15 @@ void launch_rb(const FftPassArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream) {
+    const size_t smem = size_t(1024) * (8 + 4 + 1) * sizeof(double2) + 16;
+    MNB_CUDA(cudaFuncSetAttribute(fft1024_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, a.num_sms)));
+    fft1024_select_kernel<<<grid, 512, smem, stream>>>(a, off, ent);
+    MNB_LAUNCH_CHECK();
+}
 
 bool plan_radices(int N, int& E, int* radix, int& nradix) {
     int m = N, p2 = 0, p3 = 0;

@@ -174,7 +174,8 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
 // (see HChainArgs::blk_n1): pass A (length n2, twiddled) -> tmp (blocked for
 // pass B), pass B (length n1) keeps the sampled frequencies -> out.
 void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, double2* tmp, double2* out,
-                      int64_t ld_out, int64_t out_row0, const int32_t* sel, double* ms_a, double* ms_b) {
+                      int64_t ld_out, int64_t out_row0, const int32_t* sel, const int32_t* fb_csr, double* ms_a,
+                      double* ms_b) {
     FftPlan& P = ctx.fft_plan(n);
     {
         FftPassArgs a = base_args(P.A);
@@ -211,7 +212,9 @@ void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, 
         a.rows = rows;
         a.batches = P.n2;
         EventTimer t(ctx, ms_b, 3);
-        launch_fft_pass(a, ctx.stream);
+        const bool pruned = fb_csr && P.B.N == 1024 && !P.B.direct;
+        if (pruned) launch_fft1024_select(a, fb_csr, fb_csr + P.n2 + 1, ctx.stream);
+        else launch_fft_pass(a, ctx.stream);
         ctx.launches += 1;
         t.stop();
     }
@@ -276,6 +279,33 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
                        dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
     build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
     ctx.launches += 2;
+    // kept frequencies grouped by f2 = F mod n2 for the pruned pass B (first occurrence of each F;
+    // repeated samples are copied afterwards, launch_copy_dups)
+    const FftPlan& P = ctx.fft_plan(n);
+    dev.fb_n2 = 0;
+    if (!P.single) {
+        const int64_t n2 = P.n2;
+        const int64_t* s64 = op.at<int64_t>(op.off_sample64);
+        const int32_t* sel = op.at<int32_t>(op.off_sel);
+        std::vector<int32_t> csr(size_t(n2 + 1) + 2 * size_t(op.l), 0);
+        int32_t* off = csr.data();
+        for (int64_t j = 0; j < op.l; ++j)
+            if (sel[s64[j]] == int32_t(j)) ++off[s64[j] % n2 + 1];
+        for (int64_t f2 = 0; f2 < n2; ++f2) off[f2 + 1] += off[f2];
+        std::vector<int32_t> pos(off, off + n2);
+        int32_t* ent = csr.data() + n2 + 1;
+        for (int64_t j = 0; j < op.l; ++j) {
+            const int64_t F = s64[j];
+            if (sel[F] != int32_t(j)) continue;
+            const int32_t p = pos[size_t(F % n2)]++;
+            ent[2 * p] = int32_t(F / n2);
+            ent[2 * p + 1] = int32_t(j);
+        }
+        dev.fb_csr.ensure(csr.size() * 4);
+        MNB_CUDA(cudaMemcpyAsync(dev.fb_csr.p, csr.data(), csr.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // csr is pageable
+        dev.fb_n2 = n2;
+    }
 }
 
 static HStageArgs chain_args(const SrftDev& op, bool tilde, bool adjoint) {
@@ -405,6 +435,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         // F and S (src/srft.cpp:129-131)
         if (blocked)
             fft_rows_blocked(ctx, n, x2, rs, x1, out, ldo, out_row0 + s0, op.at<int32_t>(h.off_sel),
+                             op.fb_n2 == FP.n2 ? op.fb_csr.as<int32_t>() : nullptr,
                              kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
         else
                     fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,

@@ -74,6 +74,19 @@ def test_sketch_matches_oracle(ctx, m, n, l):
     assert rel(S, Sr) <= 1e-13
 
 
+def test_sketch_with_replacement_large_n(ctx):
+    """Repeated sample indices (RandomStream::Sampling::with_replacement) through the
+    blocked, pruned pass B at n = 2^20 (l close to n so collisions are certain)."""
+    m, n, l = 8, 1 << 20, 4096
+    A, _ = make_instance(m, n, kappa=1e3, seed=99)
+    seed = mn.derive_seed(42, 12)
+    op = mn.build_srft(l, n, seed, mn.Sampling.with_replacement)
+    ref = O.Srft.build(l, n, seed, without=False)
+    assert len(np.unique(ref.field("sample"))) < l  # the case under test: some frequencies repeat
+    ctx.set_matrix(A)
+    assert rel(op.sketch(ctx), ref.sketch(A)) <= 1e-13
+
+
 def test_sketch_real_matrix(ctx):
     A, _ = make_instance(32, 6144, kappa=1e3, seed=5, real=True)
     seed = mn.derive_seed(42, 12)

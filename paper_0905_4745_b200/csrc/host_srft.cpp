@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <exception>
+#include <mutex>
 #include <thread>
 
 #include "common_host.hpp"
@@ -62,19 +64,45 @@ void RandomStream::complex_gaussian(double* z) {
     z[0] = r * c;
     z[1] = r * s;
 }
+namespace {
+// r % b, exactly, without a 64-bit hardware division for b >= 4096: a double
+// quotient estimate (off by at most 2 there) corrected by integer arithmetic.
+inline uint64_t mod64(uint64_t r, uint64_t b) {
+    if (b < 4096) return r % b;
+    const uint64_t q = uint64_t(double(r) / double(b));
+    int64_t rem = int64_t(r - q * b);
+    while (rem < 0) rem += int64_t(b);
+    while (rem >= int64_t(b)) rem -= int64_t(b);
+    return uint64_t(rem);
+}
+}  // namespace
+
 uint64_t RandomStream::uniform_below(uint64_t bound) {
     if (bound == 0) throw Error(MNB_ERR_INVALID_ARGUMENT, "uniform_below: bound must be positive");
-    const uint64_t threshold = (0 - bound) % bound;
+    // rng.cpp:79-87: accept r >= (0 - bound) % bound.  That threshold is below
+    // bound, so for bound <= 2^32 every r >= 2^32 is accepted without computing it.
     for (;;) {
         const uint64_t r = next_u64();
-        if (r >= threshold) return r % bound;
+        if ((bound <= (uint64_t(1) << 32) && r >= (uint64_t(1) << 32)) || r >= mod64(0 - bound, bound))
+            return mod64(r, bound);
     }
 }
+// Fisher-Yates (rng.cpp:89-97) with the draws taken in blocks of 64 (same
+// stream order) and the swap targets prefetched: the swaps are applied in the
+// reference's order, so the permutation is bit-identical; only the cache
+// misses of the random p[j] accesses overlap.
 void RandomStream::permutation(int32_t* p, int64_t n) {
     for (int64_t i = 0; i < n; ++i) p[i] = int32_t(i);
-    for (int64_t i = n; i > 1; --i) {
-        const int64_t j = int64_t(uniform_below(uint64_t(i)));
-        std::swap(p[i - 1], p[j]);
+    constexpr int kBlock = 64;
+    uint32_t js[kBlock];
+    for (int64_t i = n; i > 1;) {
+        const int cnt = int(std::min<int64_t>(kBlock, i - 1));
+        for (int k = 0; k < cnt; ++k) {
+            js[k] = uint32_t(uniform_below(uint64_t(i - k)));
+            __builtin_prefetch(p + js[k], 1);
+        }
+        for (int k = 0; k < cnt; ++k) std::swap(p[i - 1 - k], p[js[k]]);
+        i -= cnt;
     }
 }
 void RandomStream::sample_indices(int64_t* out, int64_t l, int64_t n, bool without) {
@@ -129,7 +157,11 @@ void SrftHost::layout() {
 // that the neglected contribution is below kHaloThreshold (the carry of the
 // chain recurrence decays by |sin(theta_j)| per step).
 static void chain_halos(const double* cssn, int64_t n, const ChainChunks& ch, int32_t* fwd, int32_t* adj) {
-    for (int64_t c = 0; c < ch.nchunks; ++c) {
+    const int threads = int(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+    for (int64_t c = t; c < ch.nchunks; c += threads) {
         const int64_t i0 = c * ch.chunk, i1 = std::min(n, i0 + ch.chunk);
         // forward chain: carry flows from high to low indices
         int64_t t = i1;
@@ -145,6 +177,8 @@ static void chain_halos(const double* cssn, int64_t n, const ChainChunks& ch, in
         while (s > 0 && p > kHaloThreshold) { --s; p *= std::fabs(cssn[2 * s + 1]); }
         adj[c] = int32_t(s);
     }
+        });
+    for (auto& th : pool) th.join();
 }
 
 void SrftHost::derive() {
@@ -216,53 +250,90 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     const RandomStream stream(stream_seed);
     const bool without = sampling == MNB_WITHOUT_REPLACEMENT;
 
-    // Phase 1: the eight tagged substreams, concurrently.  Unit-circle draws
-    // stash the angle phi in the real slot; phase 2 turns it into e^{i phi}.
+    // The eight tagged substreams are drawn concurrently (each stream is
+    // sequential, as RandomStream requires); the cos/sin of every unit-circle
+    // and rotation angle (unit_circle, rng.cpp:62-65; finalize, srft.cpp:80-93)
+    // is split into blocks that any idle worker takes as soon as that stream
+    // has been drawn, so the two serial Fisher-Yates permutations overlap the
+    // libm work.  Unit-circle draws stash phi in the real slot first.
     double* d = op.at<double>(op.off_d);
     double* zeta = op.at<double>(op.off_zeta);
     double* zeta_t = op.at<double>(op.off_zeta_tilde);
     double* theta = op.at<double>(op.off_theta);
     double* theta_t = op.at<double>(op.off_theta_tilde);
+    double* cssn = op.at<double>(op.off_cssn);
+    double* cssn_t = op.at<double>(op.off_cssn_tilde);
     auto angles_into = [&](RandomStream s, double* out, int64_t count, int64_t stride) {
         for (int64_t i = 0; i < count; ++i) out[i * stride] = s.uniform_angle();
     };
-    parallel_for(8, threads, [&](int64_t task) {
-        switch (task) {
-            case 0: angles_into(stream.substream(kD), d, n, 2); break;
-            case 1: {
-                RandomStream s = stream.substream(kSample);
-                s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
-            } break;
-            case 2: angles_into(stream.substream(kTheta), theta, n - 1, 1); break;
-            case 3: angles_into(stream.substream(kThetaTilde), theta_t, n - 1, 1); break;
-            case 4: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
-            case 5: { RandomStream s = stream.substream(kPermTilde); s.permutation(op.at<int32_t>(op.off_perm_tilde), n); } break;
-            case 6: angles_into(stream.substream(kZeta), zeta, n, 2); break;
-            case 7: angles_into(stream.substream(kZetaTilde), zeta_t, n, 2); break;
-        }
-    });
-    // Phase 2: sincos of all angles (unit_circle, rng.cpp:62-65; finalize, srft.cpp:80-93).
-    double* cssn = op.at<double>(op.off_cssn);
-    double* cssn_t = op.at<double>(op.off_cssn_tilde);
-    const int64_t blk = 1 << 15;
+    constexpr int64_t blk = 1 << 15;
     const int64_t nb = (n + blk - 1) / blk;
-    parallel_for(5 * nb, threads, [&](int64_t task) {
-        const int64_t which = task / nb, b0 = (task % nb) * blk;
-        if (which < 3) {
-            double* z = which == 0 ? d : which == 1 ? zeta : zeta_t;
+    // angle stream k: 0 d, 1 zeta, 2 zeta~ (unit circle, in place); 3 theta, 4 theta~ (-> cssn)
+    auto sincos_block = [&](int k, int64_t b0) {
+        if (k < 3) {
+            double* z = k == 0 ? d : k == 1 ? zeta : zeta_t;
             const int64_t e = std::min(n, b0 + blk);
             for (int64_t i = b0; i < e; ++i) {
                 const double phi = z[2 * i];
                 ::sincos(phi, &z[2 * i + 1], &z[2 * i]);
             }
         } else {
-            const double* th = which == 3 ? theta : theta_t;
-            double* cs = which == 3 ? cssn : cssn_t;
+            const double* th = k == 3 ? theta : theta_t;
+            double* cs = k == 3 ? cssn : cssn_t;
             const int64_t e = std::min(n - 1, b0 + blk);
             for (int64_t i = b0; i < e; ++i) ::sincos(th[i], &cs[2 * i + 1], &cs[2 * i]);
-            if (e == n - 1 && b0 <= n - 1) { cs[2 * (n - 1)] = 1.0; cs[2 * (n - 1) + 1] = 0.0; }
+            if (e == n - 1 && b0 <= n - 1) {
+                cs[2 * (n - 1)] = 1.0;
+                cs[2 * (n - 1) + 1] = 0.0;
+            }
         }
-    });
+    };
+    std::atomic<int> next_draw{0};
+    std::atomic<int> drawn[5];
+    std::atomic<int64_t> next_blk[5];
+    for (int k = 0; k < 5; ++k) {
+        drawn[k] = 0;
+        next_blk[k] = 0;
+    }
+    std::atomic<bool> failed{false};
+    std::exception_ptr error;
+    std::mutex error_mu;
+    auto worker = [&] {
+        try {
+            for (int t; (t = next_draw.fetch_add(1)) < 8;) {
+                switch (t) {  // longest first
+                    case 0: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
+                    case 1: { RandomStream s = stream.substream(kPermTilde); s.permutation(op.at<int32_t>(op.off_perm_tilde), n); } break;
+                    case 2: {
+                        RandomStream s = stream.substream(kSample);
+                        s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
+                    } break;
+                    case 3: angles_into(stream.substream(kThetaTilde), theta_t, n - 1, 1); drawn[4] = 1; break;
+                    case 4: angles_into(stream.substream(kTheta), theta, n - 1, 1); drawn[3] = 1; break;
+                    case 5: angles_into(stream.substream(kZetaTilde), zeta_t, n, 2); drawn[2] = 1; break;
+                    case 6: angles_into(stream.substream(kZeta), zeta, n, 2); drawn[1] = 1; break;
+                    case 7: angles_into(stream.substream(kD), d, n, 2); drawn[0] = 1; break;
+                }
+            }
+            for (int k : {4, 3, 2, 1, 0}) {
+                while (!drawn[k].load() && !failed.load()) std::this_thread::yield();
+                if (failed.load()) return;
+                for (int64_t b; (b = next_blk[k].fetch_add(1)) < nb;) sincos_block(k, b * blk);
+            }
+        } catch (...) {
+            std::lock_guard<std::mutex> g(error_mu);
+            if (!error) error = std::current_exception();
+            failed = true;
+        }
+    };
+    {
+        const int nt = std::max(1, threads);
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
+        worker();
+        for (auto& th : pool) th.join();
+    }
+    if (error) std::rethrow_exception(error);
     op.derive();
 }
 

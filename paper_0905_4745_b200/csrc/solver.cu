@@ -423,25 +423,21 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const RandomStream root(cfg.seed);
     const uint64_t seed_T = root.derive_seed(11), seed_Tp = root.derive_seed(12);  // src/solver.cpp:19
     const int hw = int(std::max(2u, std::thread::hardware_concurrency()));
-    // Both operators are drawn concurrently on the host; T' overlaps Steps 1-3 on the GPU.
+    // T (needed first) is drawn with every host thread; T' is drawn in the
+    // background with half of them while this thread drives Steps 1-3 on the GPU.
     SrftHost T, Tp;
     auto noop = [](unsigned char*) {};
-    const double tp0 = now_s();
     double t_param_T = 0.0, t_param_Tp = 0.0;
+    const double tp0 = now_s();
+    build_srft_host(T, l, n, seed_T, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); },
+                    noop, hw);
+    t_param_T = now_s() - tp0;
     auto fut_Tp = std::async(std::launch::async, [&] {
         const double s = now_s();
         build_srft_host(Tp, l, n, seed_Tp, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); },
-                        noop, hw / 2);
+                        noop, std::max(1, hw / 2));
         t_param_Tp = now_s() - s;
     });
-    try {
-        build_srft_host(T, l, n, seed_T, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); },
-                        noop, hw - hw / 2);
-    } catch (...) {
-        fut_Tp.wait();
-        throw;
-    }
-    t_param_T = now_s() - tp0;
 
     // ---- Step 1: S = T A^*
     double t0 = now_s();

@@ -200,6 +200,8 @@ struct FftCta {
 
     __device__ __forceinline__ double2 gload(int idx) const {
         if (!row_ok) return make_double2(0.0, 0.0);
+        if (a.blocked)  // tile of unit (row block, b) is [N][8] at in + ((row/8)*batches + b)*N*8
+            return __ldg(a.in + (((row >> 3) * a.batches + b) * a.N + idx) * 8 + (row & 7));
         const int64_t col = b * a.in_bstride + int64_t(idx) * a.in_istride;
         return __ldg(a.in + (a.in_row0 + row) + col * a.ld_in);
     }
@@ -211,8 +213,8 @@ struct FftCta {
             double2 w = c_mul(__ldg(a.tw4_hi + (e >> a.tw4_shift)), __ldg(a.tw4_lo + (e & ((int64_t(1) << a.tw4_shift) - 1))));
             if (INV) w.y = -w.y;
             v = c_mul(v, w);
-            if (a.blocked) {  // [row block][f][b][Rb]: the next pass reads one contiguous tile
-                a.out[((rbk * a.N + f) * a.batches + b) * Rb + r] = v;
+            if (a.blocked) {  // [row block][f][b][8]: the next pass reads one contiguous tile
+                a.out[(((row >> 3) * a.N + f) * a.batches + b) * 8 + (row & 7)] = v;
                 return;
             }
             const int64_t col = int64_t(f) * a.out_fstride + b * a.out_bstride;
@@ -706,7 +708,7 @@ void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
                 return;
             }
         }
-        if constexpr (Rb == 8) {
+        if constexpr (Rb == 8) if (size_t(a.N) * 12 * 16 + 16 <= size_t(227 * 1024)) {
             auto kern = a.inverse ? fft_tile_kernel<E, true> : fft_tile_kernel<E, false>;
             const size_t sm_total = size_t(a.N) * 12 * sizeof(double2) + 16;  // tile + half exchange + barrier
             MNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_total)));
@@ -720,7 +722,7 @@ void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
             MNB_LAUNCH_CHECK();
             return;
         }
-        throw Error(MNB_ERR_INTERNAL, "fft: blocked passes use 8-row tiles");
+        // otherwise: the generic kernel below, addressing the blocked layout (half or quarter 8-row blocks)
     }
     dim3 grid(ceil_div(a.rows, Rb), unsigned(a.batches));
     // Clusters of adjacent row blocks are co-scheduled, so the DRAM sees the

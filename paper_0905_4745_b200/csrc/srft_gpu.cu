@@ -188,7 +188,7 @@ void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, 
         a.tw4_lo = P.tw4_lo.as<double2>();
         a.tw4_shift = P.tw4_shift;
         a.n_total = n;
-        a.Rb = 8;
+        a.Rb = fft_tile_fits(P.A.N, P.A.E) ? 8 : std::min(4, rows_per_cta(P.A));
         a.rows = rows;
         a.batches = P.n1;
         EventTimer t(ctx, ms_a, 2);
@@ -208,11 +208,11 @@ void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, 
         a.nb = P.n2;
         a.sel = sel;
         a.scale = 1.0 / std::sqrt(double(n));
-        a.Rb = 8;
+        a.Rb = fft_tile_fits(P.B.N, P.B.E) ? 8 : std::min(4, rows_per_cta(P.B));
         a.rows = rows;
         a.batches = P.n2;
         EventTimer t(ctx, ms_b, 3);
-        const bool pruned = fb_csr && P.B.N == 1024 && !P.B.direct;
+        const bool pruned = fb_csr && P.B.N == 1024 && !P.B.direct && a.Rb == 8;
         if (pruned) launch_fft1024_select(a, fb_csr, fb_csr + P.n2 + 1, ctx.stream);
         else launch_fft_pass(a, ctx.stream);
         ctx.launches += 1;
@@ -345,6 +345,8 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
     const FftPlan& FP = ctx.fft_plan(n);
     // Four-step FFT with both passes' tiles (8 rows x N) in shared memory: P2 writes x2 in
     // the blocked layout pass A reads as contiguous tiles, pass A writes the one pass B reads.
+    // (for longer passes, e.g. 1536 x 2048 at n = 3*2^20, the blocked layout read through 4-row
+    // halves measured slower than the plain [n][Ms] layout: keep the latter there)
     const bool blocked = hchain_fits(h.max_span, is_real) && !FP.single && !FP.A.direct && !FP.B.direct &&
                          fft_tile_fits(FP.A.N, FP.A.E) && fft_tile_fits(FP.B.N, FP.B.E);
     const double scale = 1.0 / std::sqrt(double(n));

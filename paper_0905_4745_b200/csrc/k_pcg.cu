@@ -101,7 +101,7 @@ __device__ __forceinline__ void axpy_acc<double>(double2& acc, double a, double2
 // batches (current + next) at <= 16 complex (or 32 real) values per thread.
 template <typename AT, int EPL>
 __host__ __device__ constexpr int batch_cols() {
-    return sizeof(AT) == 16 ? (EPL <= 2 ? 4 : EPL == 4 ? 2 : 1) : (EPL <= 2 ? 4 : EPL == 4 ? 2 : 1);
+    return sizeof(AT) == 16 ? (EPL <= 2 ? 4 : EPL == 4 ? 2 : 1) : (EPL <= 4 ? 4 : 2);
 }
 
 struct SmemLayout {

@@ -77,6 +77,8 @@ struct SrftDev {
     DevBuf dups;
     int64_t ndups = 0;
     DevBuf chain_rec[2];  // per-step chain records of the sketch H stages: [0] P1 (tilde half), [1] P2
+    DevBuf vec_halo;      // restart points of 64-index chunks for single-vector chains: fwd, fwd~, adj, adj~
+    int64_t vec_chunk = 0, vec_nchunks = 0;
     DevBuf fb_csr;        // kept frequencies per f2 for the pruned FFT pass B: [n2+1 offsets][(f1, slot) pairs]
     int64_t fb_n2 = 0;
     template <class T> const T* at(size_t off) const { return reinterpret_cast<const T*>(blob.as<unsigned char>() + off); }

@@ -96,4 +96,32 @@ void launch_max_offset_from_identity(const double2* A, int64_t m, double* out, c
     MNB_LAUNCH_CHECK();
 }
 
+// Chain restart points for chunks of `chunk` indices (host_srft.cpp chain_halos,
+// same 2^-70 rule) -- finer chunks than the operator's, for single vectors.
+__global__ void chain_halo_kernel(const double2* __restrict__ cssn, int64_t n, int64_t chunk, int64_t nchunks,
+                                  int32_t* fwd, int32_t* adj) {
+    const int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    constexpr double thr = 0x1.0p-70;
+    const int64_t i0 = c * chunk, i1 = min(n, i0 + chunk);
+    int64_t t = i1;
+    if (i1 >= n) {
+        t = n - 1;
+    } else {
+        double p = 1.0;
+        while (t < n - 1 && p > thr) { p *= fabs(cssn[t].y); ++t; }
+    }
+    fwd[c] = int32_t(t);
+    int64_t s = i0;
+    double p = 1.0;
+    while (s > 0 && p > thr) { --s; p *= fabs(cssn[s].y); }
+    adj[c] = int32_t(s);
+}
+
+void launch_chain_halos(const double2* cssn, int64_t n, int64_t chunk, int64_t nchunks, int32_t* fwd, int32_t* adj,
+                        cudaStream_t stream) {
+    chain_halo_kernel<<<ceil_div(nchunks, 128), 128, 0, stream>>>(cssn, n, chunk, nchunks, fwd, adj);
+    MNB_LAUNCH_CHECK();
+}
+
 }  // namespace mnb

@@ -93,6 +93,9 @@ void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream);
 bool plan_radices(int N, int& E, int* radix, int& nradix);
 
 // ---------------------------------------------------------------- misc
+// chain restart points for chunks of `chunk` indices (forward and adjoint chains)
+void launch_chain_halos(const double2* cssn, int64_t n, int64_t chunk, int64_t nchunks, int32_t* fwd, int32_t* adj,
+                        cudaStream_t stream);
 // zero the strictly lower triangle of an m x m column-major matrix
 void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream);
 // out[0] = max_{i<=j} |A_ij - delta_ij| over the upper triangle (deterministic)

@@ -279,6 +279,16 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
                        dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
     build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
     ctx.launches += 2;
+    // fine restart points for single-vector H stages (apply / apply_adjoint of one vector)
+    dev.vec_chunk = 64;
+    dev.vec_nchunks = (n + dev.vec_chunk - 1) / dev.vec_chunk;
+    {
+        int32_t* vh = static_cast<int32_t*>(dev.vec_halo.ensure(size_t(4 * dev.vec_nchunks) * 4));
+        const int64_t vc = dev.vec_nchunks;
+        launch_chain_halos(dev.at<double2>(op.off_cssn), n, dev.vec_chunk, vc, vh, vh + 2 * vc, ctx.stream);
+        launch_chain_halos(dev.at<double2>(op.off_cssn_tilde), n, dev.vec_chunk, vc, vh + vc, vh + 3 * vc, ctx.stream);
+        ctx.launches += 2;
+    }
     // kept frequencies grouped by f2 = F mod n2 for the pruned pass B (first occurrence of each F;
     // repeated samples are copied afterwards, launch_copy_dups)
     const FftPlan& P = ctx.fft_plan(n);
@@ -306,6 +316,20 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
         MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // csr is pageable
         dev.fb_n2 = n2;
     }
+}
+
+// single vectors: the operator's fine 64-index chunks (more threads than rows x 1024-chunks)
+static HStageArgs vec_chain_args(const SrftDev& op, bool tilde, bool adjoint) {
+    const SrftHost& h = *op.host;
+    HStageArgs a;
+    a.cssn = op.at<double2>(tilde ? h.off_cssn_tilde : h.off_cssn);
+    const int64_t nc = op.vec_nchunks;
+    a.halo = op.vec_halo.as<int32_t>() + (adjoint ? 2 * nc : 0) + (tilde ? nc : 0);
+    a.adjoint = adjoint ? 1 : 0;
+    a.n = h.n;
+    a.chunk = op.vec_chunk;
+    a.nchunks = nc;
+    return a;
 }
 
 static HStageArgs chain_args(const SrftDev& op, bool tilde, bool adjoint) {
@@ -553,7 +577,7 @@ void srft_adjoint_vec(Context& ctx, const SrftDev& op, const double2* v, double2
     // F^{-1} (src/srft.cpp:140)
     dft_vec_to(ctx, n, w, wf, true);
     {  // conj(D), Theta^*, Pi^*, conj(Z)   (src/srft.cpp:141, :64-66)
-        HStageArgs a = chain_args(op, false, true);
+        HStageArgs a = vec_chain_args(op, false, true);
         a.in = wf;
         a.ld_in = 1;
         a.in_diag = op.at<double2>(h.off_d);
@@ -567,7 +591,7 @@ void srft_adjoint_vec(Context& ctx, const SrftDev& op, const double2* v, double2
         launch_hstage(a, ctx.stream);
     }
     {  // Theta~^*, Pi~^*, conj(Z~)   (src/srft.cpp:67-69)
-        HStageArgs a = chain_args(op, true, true);
+        HStageArgs a = vec_chain_args(op, true, true);
         a.in = w;
         a.ld_in = 1;
         a.out = y;
@@ -587,7 +611,7 @@ void srft_apply_vec(Context& ctx, const SrftDev& op, const double2* x, double2* 
     double2* t1 = static_cast<double2*>(ctx.vec_full[0].ensure(size_t(n) * 16));
     double2* t2 = static_cast<double2*>(ctx.vec_full[1].ensure(size_t(n) * 16));
     {
-        HStageArgs a = chain_args(op, true, false);
+        HStageArgs a = vec_chain_args(op, true, false);
         a.in = x;
         a.ld_in = 1;
         a.gather = op.at<int32_t>(h.off_perm_tilde);
@@ -599,7 +623,7 @@ void srft_apply_vec(Context& ctx, const SrftDev& op, const double2* x, double2* 
         launch_hstage(a, ctx.stream);
     }
     {
-        HStageArgs a = chain_args(op, false, false);
+        HStageArgs a = vec_chain_args(op, false, false);
         a.in = t1;
         a.ld_in = 1;
         a.gather = op.at<int32_t>(h.off_perm);

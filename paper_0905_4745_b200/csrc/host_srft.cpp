@@ -64,18 +64,6 @@ void RandomStream::complex_gaussian(double* z) {
     z[0] = r * c;
     z[1] = r * s;
 }
-namespace {
-// r % b, exactly, without a 64-bit hardware division for b >= 4096: a double
-// quotient estimate (off by at most 2 there) corrected by integer arithmetic.
-inline uint64_t mod64(uint64_t r, uint64_t b) {
-    if (b < 4096) return r % b;
-    const uint64_t q = uint64_t(double(r) / double(b));
-    int64_t rem = int64_t(r - q * b);
-    while (rem < 0) rem += int64_t(b);
-    while (rem >= int64_t(b)) rem -= int64_t(b);
-    return uint64_t(rem);
-}
-}  // namespace
 
 uint64_t RandomStream::uniform_below(uint64_t bound) {
     if (bound == 0) throw Error(MNB_ERR_INVALID_ARGUMENT, "uniform_below: bound must be positive");
@@ -83,8 +71,8 @@ uint64_t RandomStream::uniform_below(uint64_t bound) {
     // bound, so for bound <= 2^32 every r >= 2^32 is accepted without computing it.
     for (;;) {
         const uint64_t r = next_u64();
-        if ((bound <= (uint64_t(1) << 32) && r >= (uint64_t(1) << 32)) || r >= mod64(0 - bound, bound))
-            return mod64(r, bound);
+        if ((bound <= (uint64_t(1) << 32) && r >= (uint64_t(1) << 32)) || r >= (0 - bound) % bound)
+            return r % bound;
     }
 }
 // Fisher-Yates (rng.cpp:89-97) with the draws taken in blocks of 64 (same

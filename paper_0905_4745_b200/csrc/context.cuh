@@ -142,6 +142,7 @@ struct LsqResult {
     bool converged = false;
     double achieved_excess = 0.0;
     double rr0 = 0.0;
+    double xx = 0.0;  // ||x||^2 when run_cg accumulated x
     std::vector<double> residual_norms;
     double pass_ms = 0.0;
     int64_t pass_launches = 0;

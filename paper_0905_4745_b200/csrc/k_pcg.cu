@@ -105,7 +105,7 @@ __host__ __device__ constexpr int batch_cols() {
 }
 
 struct SmemLayout {
-    size_t tileA, tileT, tileR, stage_bytes, red, bars, total;
+    size_t tileA, tileT, tileR, tileX, stage_bytes, red, bars, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(int64_t m, int64_t C, int esz, int stages, int V) {
@@ -114,7 +114,8 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t m, int64_t C, int esz,
     L.tileA = 0;
     L.tileT = (a + 127) & ~size_t(127);
     L.tileR = L.tileT + ((size_t(C) * 16 + 127) & ~size_t(127));
-    L.stage_bytes = L.tileR + ((size_t(C) * 16 + 127) & ~size_t(127));
+    L.tileX = L.tileR + ((size_t(C) * 16 + 127) & ~size_t(127));
+    L.stage_bytes = L.tileX + ((size_t(C) * 16 + 127) & ~size_t(127));
     L.red = size_t(stages) * L.stage_bytes;  // [groups][2 bufs][G warps][V] doubles = 2 * 16 * V doubles
     L.bars = L.red + size_t(2 * kConsumerWarps * V) * 8;
     L.total = L.bars + size_t(2 * stages) * 8;
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     const bool init = mode == PCG_INIT;
     const bool need_t = init || mode == PCG_CG;
     const bool need_r = mode == PCG_CG;
+    const bool need_x = mode == PCG_CG && p.x != nullptr;  // x = sum_k alpha_k t_k, updated lagged like r
     const double alpha_prev = (mode == PCG_CG && p.state) ? p.state->alpha : 0.0;
 
     if (threadIdx.x == 0) {
@@ -205,10 +207,11 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
         if (abytes != abulk)  // odd real tail: 8 bytes by hand, published by the arrive below
             *reinterpret_cast<double*>(st + L.tileA + abulk) = __ldg(reinterpret_cast<const double*>(src + abulk));
         const uint32_t vbytes = uint32_t(cc * 16);
-        mbar_expect_tx(&full[slot], abulk + (need_t ? vbytes : 0u) + (need_r ? vbytes : 0u));
+        mbar_expect_tx(&full[slot], abulk + (need_t ? vbytes : 0u) + (need_r ? vbytes : 0u) + (need_x ? vbytes : 0u));
         if (abulk) bulk_g2s(st + L.tileA, src, abulk, &full[slot]);
         if (need_t) bulk_g2s(st + L.tileT, p.tin + c0, vbytes, &full[slot]);
         if (need_r) bulk_g2s(st + L.tileR, p.r + c0, vbytes, &full[slot]);
+        if (need_x) bulk_g2s(st + L.tileX, p.x + c0, vbytes, &full[slot]);
     };
     if (threadIdx.x == 0)
         for (int s = 0; s < nstage && s < stages; ++s) produce(s, s);
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
             const unsigned char* cst = smem + cslot * L.stage_bytes;
             const double2* tT = reinterpret_cast<const double2*>(cst + L.tileT) + gq * K;
             const double2* tR = reinterpret_cast<const double2*>(cst + L.tileR) + gq * K;
+            const double2* tX = reinterpret_cast<const double2*>(cst + L.tileX) + gq * K;
             double2 t[K];
             if (init) {
                 const int have = int(cc) - gq * K;
@@ -343,9 +347,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
                     rt = fma(rk.x, tk.x, fma(rk.y, tk.y, rt));  // Re(conj(r) t)
                     p.r[col] = rk;
                     p.tout[col] = tk;
+                    if (need_x) {
+                        double2 xk = tX[lane];
+                        xk.x = fma(alpha_prev, told.x, xk.x);
+                        xk.y = fma(alpha_prev, told.y, xk.y);
+                        p.x[col] = xk;
+                    }
                 } else if (init) {
                     p.r[col] = tk;
                     p.tout[col] = make_double2(0.0, 0.0);
+                    if (p.x) p.x[col] = make_double2(0.0, 0.0);
                 } else {
                     p.tout[col] = tk;
                 }
@@ -449,7 +460,7 @@ __global__ void __launch_bounds__(kUpdWarps * 32) pcg_upd1_kernel(const double* 
                                                                  const double2* __restrict__ Rinv, int64_t m,
                                                                  double2* u, double2* g, const double2* dir,
                                                                  double2* dir_old, double* part_gg, CgState* st,
-                                                                 double* residual_norms, int init) {
+                                                                 double* residual_norms, int init, double2* ax) {
     extern __shared__ double2 s_sh[];
     __shared__ double wsum[kUpdWarps];
     if (st->done) return;
@@ -489,7 +500,14 @@ __global__ void __launch_bounds__(kUpdWarps * 32) pcg_upd1_kernel(const double* 
                 gj = acc;
                 u[j] = make_double2(0.0, 0.0);
                 dir_old[j] = make_double2(0.0, 0.0);
+                if (ax) ax[j] = make_double2(0.0, 0.0);
             } else {
+                if (ax) {  // A x = sum_k alpha_k s_k (the Step-5 product, src/solver.cpp:122)
+                    double2 axj = ax[j];
+                    axj.x = fma(alpha, s_sh[j].x, axj.x);
+                    axj.y = fma(alpha, s_sh[j].y, axj.y);
+                    ax[j] = axj;
+                }
                 const double2 dj = dir[j];
                 double2 uj = u[j];
                 uj.x = fma(alpha, dj.x, uj.x);
@@ -581,33 +599,57 @@ __global__ void __launch_bounds__(kUpdWarps * 32) pcg_upd2_kernel(const double* 
 }
 
 // finalize: apply the pending lagged update and take the exact ||r||^2.
-__global__ void pcg_finalize_kernel(double2* r, const double2* t, int64_t n, const CgState* st, double* scratch) {
-    __shared__ double ws[32];
+__global__ void pcg_finalize_kernel(double2* r, const double2* t, double2* x, int64_t n, const CgState* st,
+                                    double* scratch) {
+    __shared__ double ws[32], wx[32];
     const double alpha = st->alpha;
-    double acc = 0.0;
+    double acc = 0.0, accx = 0.0;
     for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < n; k += int64_t(gridDim.x) * blockDim.x) {
         double2 rk = r[k];
+        const double2 tk = alpha != 0.0 ? t[k] : make_double2(0.0, 0.0);
         if (alpha != 0.0) {
-            const double2 tk = t[k];
             rk.x = fma(-alpha, tk.x, rk.x);
             rk.y = fma(-alpha, tk.y, rk.y);
             r[k] = rk;
         }
         acc = fma(rk.x, rk.x, fma(rk.y, rk.y, acc));
+        if (x) {
+            double2 xk = x[k];
+            if (alpha != 0.0) {
+                xk.x = fma(alpha, tk.x, xk.x);
+                xk.y = fma(alpha, tk.y, xk.y);
+                x[k] = xk;
+            }
+            accx = fma(xk.x, xk.x, fma(xk.y, xk.y, accx));
+        }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        accx += __shfl_xor_sync(0xffffffffu, accx, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        ws[threadIdx.x >> 5] = acc;
+        wx[threadIdx.x >> 5] = accx;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < int(blockDim.x >> 5); ++w) s += ws[w];
-        scratch[blockIdx.x] = s;
+        double s = 0.0, sx = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+            s += ws[w];
+            sx += wx[w];
+        }
+        scratch[2 * blockIdx.x] = s;
+        scratch[2 * blockIdx.x + 1] = sx;
     }
 }
 __global__ void pcg_finalize_sum_kernel(const double* scratch, int parts, CgState* st) {
-    double s = 0.0;
-    for (int b = 0; b < parts; ++b) s += scratch[b];
+    double s = 0.0, sx = 0.0;
+    for (int b = 0; b < parts; ++b) {
+        s += scratch[2 * b];
+        sx += scratch[2 * b + 1];
+    }
     st->rr_final = s;
+    st->xx_final = sx;
     st->alpha = 0.0;
 }
 
@@ -748,12 +790,12 @@ int pcg_upd_blocks(int64_t m) { return int(ceil_div(m, kUpdWarps)); }
 
 void launch_pcg_upd1(const double* red, const double2* Rinv, int64_t m, double2* u, double2* g, const double2* dir,
                      double2* dir_old, double* part_gg, CgState* state, double* residual_norms, int init,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, double2* ax) {
     const size_t smem = size_t(m) * 16;
     if (smem > 48 * 1024)
         MNB_CUDA(cudaFuncSetAttribute(pcg_upd1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     pcg_upd1_kernel<<<pcg_upd_blocks(m), kUpdWarps * 32, smem, stream>>>(red, Rinv, m, u, g, dir, dir_old, part_gg,
-                                                                       state, residual_norms, init);
+                                                                       state, residual_norms, init, ax);
     MNB_LAUNCH_CHECK();
 }
 
@@ -768,10 +810,10 @@ void launch_pcg_upd2(const double* part_gg, int parts_gg, const double2* Rinv_ro
     MNB_LAUNCH_CHECK();
 }
 
-void launch_pcg_finalize(double2* r, const double2* t, int64_t n, CgState* state, double* scratch,
+void launch_pcg_finalize(double2* r, const double2* t, double2* x, int64_t n, CgState* state, double* scratch,
                          cudaStream_t stream) {
     const int blocks = int(std::min<int64_t>(296, ceil_div(n, 256)));
-    pcg_finalize_kernel<<<blocks, 256, 0, stream>>>(r, t, n, state, scratch);
+    pcg_finalize_kernel<<<blocks, 256, 0, stream>>>(r, t, x, n, state, scratch);
     MNB_LAUNCH_CHECK();
     pcg_finalize_sum_kernel<<<1, 1, 0, stream>>>(scratch, blocks, state);
     MNB_LAUNCH_CHECK();

@@ -17,6 +17,7 @@ struct CgState {
     double dup;       // max multiplicity (lsq.cpp:70)
     double excess;    // dup * gg at the last convergence test
     double rr_final;  // exact ||r||^2 of the returned iterate (finalize)
+    double xx_final;  // ||x||^2 of x = sum_k alpha_k t_k (finalize; the Step-5 vector)
     long long iterations;
     long long max_iterations;
     int done;
@@ -39,6 +40,7 @@ struct PcgPassArgs {
     const double2* tin = nullptr;  // n (INIT: c; CG: t_{k-1})
     double2* tout = nullptr;       // n (CG: same as tin; APPLY: x)
     double2* r = nullptr;          // n
+    double2* x = nullptr;          // n or null: x += alpha_prev t_prev (CG), x = 0 (INIT)
     const CgState* state = nullptr;
     double2* part_s = nullptr;     // [grid][m]
     double* part_scal = nullptr;   // [grid][4]: qq, Re<r,t>, ||r||^2, -
@@ -61,14 +63,14 @@ void launch_pcg_reduce(const double2* part_s, const double* part_scal, int parts
 // upd1: alpha = gg/qq; u += alpha dir; g -= alpha Rinv^H s; dir_old = dir; part_gg
 void launch_pcg_upd1(const double* red, const double2* Rinv, int64_t m, double2* u, double2* g, const double2* dir,
                      double2* dir_old, double* part_gg, CgState* state, double* residual_norms, int init,
-                     cudaStream_t stream);
+                     cudaStream_t stream, double2* ax = nullptr);
 // upd2: gg' = sum part_gg; convergence; dir = g + beta dir_old; w = Rinv dir
 void launch_pcg_upd2(const double* part_gg, int parts_gg, const double2* Rinv_rows, int64_t m, const double2* g,
                      const double2* dir_old, double2* dir, double2* w, CgState* state, int init,
                      cudaStream_t stream);
 int pcg_upd_blocks(int64_t m);
-// r <- r - alpha t (pending update), ||r||^2 -> state->rr_final
-void launch_pcg_finalize(double2* r, const double2* t, int64_t n, CgState* state, double* scratch,
+// r <- r - alpha t, x <- x + alpha t (pending updates), ||r||^2 -> rr_final, ||x||^2 -> xx_final
+void launch_pcg_finalize(double2* r, const double2* t, double2* x, int64_t n, CgState* state, double* scratch,
                          cudaStream_t stream);
 // y = Rinv u (upper triangular, row layout)
 void launch_trmv_rows(const double2* Rinv_rows, int64_t m, const double2* u, double2* y, cudaStream_t stream);

@@ -97,7 +97,7 @@ PassBuffers pass_buffers(Context& ctx) {
 
 // One fused pass + deterministic reduction (+ allreduce across ranks).
 void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w, const double2* tin, double2* tout,
-                double2* r, const CgState* state) {
+                double2* r, const CgState* state, double2* x = nullptr) {
     if (ctx.n_local > 0) {
         PcgPassArgs a;
         a.A = ctx.A;
@@ -108,6 +108,7 @@ void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w,
         a.tin = tin;
         a.tout = tout;
         a.r = r;
+        a.x = x;
         a.state = state;
         a.part_s = pb.part_s;
         a.part_scal = pb.part_scal;
@@ -146,8 +147,10 @@ cudaEvent_t Context::event(size_t i) {
 // ------------------------------------------------------------- CG loop ----
 // solve_least_squares (src/lsq.cpp:43-113) from the sketch R' onward.
 // c: this rank's n_local entries (device).  y: m entries (device).
+// x, ax (optional): also accumulate x = A^H y = sum_k alpha_k t_k (this rank's columns) and
+// A x = sum_k alpha_k s_k inside the CG passes, so Step 5 (src/solver.cpp:118-125) needs no extra pass.
 LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
-                 double dup, double2* y, bool want_norms) {
+                 double dup, double2* y, bool want_norms, double2* x, double2* ax) {
     const int64_t m = ctx.m, n = ctx.n_local;
     LsqResult res;
     const double t0 = now_s();
@@ -187,9 +190,9 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     // initial state (lsq.cpp:77-86): r = c, g = M^H c, dir = g
     cudaEvent_t ea = ctx.event(20), eb = ctx.event(21);
     MNB_CUDA(cudaEventRecord(ea, ctx.stream));
-    fused_pass(ctx, pb, PCG_INIT, nullptr, c, t, r, nullptr);
+    fused_pass(ctx, pb, PCG_INIT, nullptr, c, t, r, nullptr, x);
     MNB_CUDA(cudaEventRecord(eb, ctx.stream));
-    launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 1, ctx.stream);
+    launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 1, ctx.stream, ax);
     launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 1, ctx.stream);
     ctx.launches += 3;
 
@@ -210,30 +213,31 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
         for (int64_t k = 0; k < K; ++k) {
             cudaEvent_t e0 = ctx.event(32 + 2 * size_t(issued)), e1 = ctx.event(33 + 2 * size_t(issued));
             MNB_CUDA(cudaEventRecord(e0, ctx.stream));
-            fused_pass(ctx, pb, PCG_CG, w, t, t, r, st);
+            fused_pass(ctx, pb, PCG_CG, w, t, t, r, st, x);
             MNB_CUDA(cudaEventRecord(e1, ctx.stream));
             pass_ev.emplace_back(e0, e1);
-            launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 0, ctx.stream);
+            launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 0, ctx.stream, ax);
             launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 0, ctx.stream);
             ctx.launches += 2;
             ++issued;
         }
     }
     // exact final residual and y = R'^{-1} u (lsq.cpp:109-111)
-    double* scratch = dev<double>(ctx.scratch, 512);
+    double* scratch = dev<double>(ctx.scratch, 1024);
     if (n > 0) {
-        launch_pcg_finalize(r, t, n, st, scratch, ctx.stream);
+        launch_pcg_finalize(r, t, x, n, st, scratch, ctx.stream);
         ctx.launches += 2;
     } else {
-        MNB_CUDA(cudaMemsetAsync(&st->rr_final, 0, 8, ctx.stream));
+        MNB_CUDA(cudaMemsetAsync(&st->rr_final, 0, 16, ctx.stream));
     }
-    allreduce_sum(ctx, &st->rr_final, 1);
+    allreduce_sum(ctx, &st->rr_final, 2);  // rr_final, xx_final
     launch_trmv_rows(Rinv_rows, m, u, y, ctx.stream);
     ctx.launches += 1;
     read_state();
     res.iterations = st_h->iterations;
     res.converged = st_h->converged != 0;
     res.rr0 = st_h->rr0;
+    res.xx = st_h->xx_final;
     const double rr = st_h->rr_final, excess = st_h->excess;
     const double min_est = std::max(rr - excess, 0.0);
     res.achieved_excess = min_est > 0.0 ? excess / min_est : 0.0;
@@ -540,7 +544,9 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                     "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
-    LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false);
+    double2* ax = dev<double2>(ctx.vec_m[7], size_t(m));
+    LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false,
+                          ctx.n_local ? x_dev : nullptr, ax);
     rep.lsq_iterations = ls.iterations;
     rep.lsq_converged = ls.converged ? 1 : 0;
     rep.lsq_achieved_excess = ls.achieved_excess;
@@ -549,24 +555,23 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.pcg_pass_launches = ls.pass_launches;
     rep.step_seconds[3] = now_s() - t0;
 
-    // ---- Step 5: x = A^* y, residual ||A x - b|| (src/solver.cpp:118-125)
+    // ---- Step 5: x = A^* y, residual ||A x - b|| (src/solver.cpp:118-125).  x and A x were
+    // accumulated inside the CG passes (x = sum_k alpha_k t_k, A x = sum_k alpha_k s_k): no extra pass.
     t0 = now_s();
-    PassBuffers pb = pass_buffers(ctx);
-    fused_pass(ctx, pb, PCG_APPLY, y, nullptr, x_dev, nullptr, nullptr);
-    std::vector<double> red(size_t(2 * m + 4));
-    MNB_CUDA(cudaMemcpyAsync(red.data(), pb.red, red.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    std::vector<double> axh(size_t(2 * m));
+    MNB_CUDA(cudaMemcpyAsync(axh.data(), ax, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
     if (c_dev && ctx.n_local)
         MNB_CUDA(cudaMemcpyAsync(c_dev, c_loc, size_t(ctx.n_local) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     sync(ctx);
     rep.step_seconds[4] = now_s() - t0;
     double res2 = 0.0;
     for (int64_t i = 0; i < m; ++i) {
-        const double dr = red[size_t(2 * i)] - reinterpret_cast<const double*>(b_host)[2 * i];
-        const double di = red[size_t(2 * i + 1)] - reinterpret_cast<const double*>(b_host)[2 * i + 1];
+        const double dr = axh[size_t(2 * i)] - reinterpret_cast<const double*>(b_host)[2 * i];
+        const double di = axh[size_t(2 * i + 1)] - reinterpret_cast<const double*>(b_host)[2 * i + 1];
         res2 += dr * dr + di * di;
     }
     rep.residual_norm = std::sqrt(res2);
-    const double xnorm = std::sqrt(red[size_t(2 * m)]);
+    const double xnorm = std::sqrt(ls.xx);
     rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
     rep.kernel_launches = ctx.launches - launches0;
     rep.total_seconds = now_s() - t_start;
@@ -596,7 +601,7 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
     LsqResult ls = run_cg(ctx, c_dev, eq.R, eq.ldR, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
-                          residual_norms != nullptr);
+                          residual_norms != nullptr, nullptr, nullptr);
     MNB_CUDA(cudaMemcpyAsync(y_host, y, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
     sync(ctx);
     sol.achieved_excess = ls.achieved_excess;

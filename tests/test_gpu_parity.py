@@ -126,6 +126,9 @@ def test_solve_randomized_matches_oracle(ctx, m, n, kappa, eps):
         # it runs lsq_max_iterations and diverges
         assert ref.lsq_iterations == 300
     assert rep.residual_norm <= 1e-6 * np.linalg.norm(b) * kappa
+    # the report's ||A x - b|| (accumulated inside the CG passes) is the residual of the returned x
+    true_res = np.linalg.norm(A @ rep.x - b)
+    assert abs(rep.residual_norm - true_res) <= 1e-3 * true_res + 1e-12 * np.linalg.norm(b) * kappa
 
 
 def test_solve_real_matrix(ctx):

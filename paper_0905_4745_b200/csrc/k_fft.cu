@@ -664,6 +664,71 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
 }
 
 
+// Pass B pruned to the sampled frequencies for the plain [n][Ms] layout and any
+// N = 16 U (U <= 128; e.g. 2048 or 1536 at n = 3*2^20): Y_u[j] = sum_q
+// x[u + U q] w_16^{j q} in registers (16 loads per thread straight from global,
+// Rb rows x U threads), then each kept frequency is X[f] = sum_u w_N^{f u}
+// Y_u[f mod 16], one warp per (row, sample) pair.  Persistent over units
+// (row block, f2); the next unit's loads are issued before the warp sums.
+__global__ void __launch_bounds__(512, 1) fft_select_pruned_kernel(const FftPassArgs a, const int32_t* __restrict__ off,
+                                                                 const int32_t* __restrict__ ent, int Rb, int U) {
+    extern __shared__ double2 sm[];
+    const int N = a.N;
+    double2* W = sm;          // w_N^k
+    double2* X = sm + N;      // [Rb][16][U]
+    const int r = int(threadIdx.x) % Rb, u = int(threadIdx.x) / Rb;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31), nwarps = int(blockDim.x >> 5);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = __ldg(a.tw + i);
+    const int64_t nrb = (a.rows + Rb - 1) / Rb;
+    const int64_t units = nrb * a.batches;
+    auto load = [&](int64_t unit, double2 (&v)[16]) {
+        const int64_t rb = unit / a.batches, b = unit - rb * a.batches;
+        const int64_t row = rb * Rb + r;
+        if (row >= a.rows) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = make_double2(0.0, 0.0);
+            return;
+        }
+        const double2* base = a.in + (a.in_row0 + row) + b * a.in_bstride * a.ld_in;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = __ldg(base + int64_t(u + U * q) * a.in_istride * a.ld_in);
+    };
+    double2 v[16];
+    int64_t unit = blockIdx.x;
+    if (unit < units) load(unit, v);
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t rb = unit / a.batches, b = unit - rb * a.batches;
+        dft16_np<false>(v);
+        __syncthreads();  // the previous unit's sums are done with X (and W is loaded)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) X[(r * 16 + j) * U + u] = v[d16(j)];
+        __syncthreads();
+        const int64_t next = unit + gridDim.x;
+        if (next < units) load(next, v);  // in flight during the sums
+        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        for (int p = warp; p < Rb * cnt; p += nwarps) {
+            const int rp = p % Rb, s = p / Rb;
+            const int f = __ldg(ent + 2 * (e0 + s)), slot = __ldg(ent + 2 * (e0 + s) + 1);
+            const double2* Y = X + (rp * 16 + (f & 15)) * U;
+            double2 acc = make_double2(0.0, 0.0);
+            for (int uu = lane; uu < U; uu += 32) {
+                const double2 y = Y[uu];
+                const double2 w = W[(int64_t(f) * uu) % N];
+                acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
+                acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+            }
+            const int64_t orow = rb * Rb + rp;
+            if (lane == 0 && orow < a.rows)
+                a.out[int64_t(slot) + (a.out_row0 + orow) * a.ld_out] = c_scale(acc, a.scale);
+        }
+    }
+}
+
 // N == 1: the transform is the identity; only the epilogue (twiddle/select) runs.
 template <bool INV>
 __global__ void fft_len1_kernel(const FftPassArgs a) {
@@ -768,6 +833,22 @@ void launch_rb(const FftPassArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
+                              cudaStream_t stream) {
+    if (a.inverse || a.N % 16 != 0 || a.N / 16 > 128) return false;
+    const int U = a.N / 16;
+    int Rb = 8;
+    while (Rb > 1 && Rb * U > 512) Rb >>= 1;
+    const size_t smem = (size_t(a.N) + size_t(Rb) * 16 * U) * sizeof(double2);
+    if (smem > size_t(227 * 1024)) return false;
+    MNB_CUDA(cudaFuncSetAttribute(fft_select_pruned_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t units = int64_t(ceil_div(a.rows, Rb)) * a.batches;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, num_sms)));
+    fft_select_pruned_kernel<<<grid, Rb * U, smem, stream>>>(a, off, ent, Rb, U);
+    MNB_LAUNCH_CHECK();
+    return true;
+}
 
 void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream) {
     const size_t smem = size_t(1024) * (8 + 4 + 1) * sizeof(double2) + 16;

@@ -86,6 +86,10 @@ void launch_fft_pass(const FftPassArgs& a, cudaStream_t stream);
 // Blocked pass B with N = 1024, pruned to the sampled frequencies: per batch f2 the CSR list
 // off[f2] .. off[f2+1] of (f1, slot) pairs in ent (forward, SELECT semantics of FftPassArgs).
 void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream);
+// Pass B pruned to the sampled frequencies, plain [n][Ms] layout, N = 16 U (U <= 128).
+// Returns false (nothing launched) when the shape is not covered.
+bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
+                              cudaStream_t stream);
 // O(N^2) fallback for lengths without a 2^a 3^b factorisation (N <= 4096).
 void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream);
 // Largest per-thread element count E (and radix plan) for an in-smem length N;

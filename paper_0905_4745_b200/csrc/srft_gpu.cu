@@ -48,7 +48,7 @@ void make_len_plan(FftLenPlan& p, int64_t N, cudaStream_t stream) {
 bool fft_tile_fits(int N, int E) { return size_t(N) * 12 * 16 + 16 <= size_t(227 * 1024) && 8 * N / E <= 512; }
 
 int rows_per_cta(const FftLenPlan& p) {
-    int rb = p.N <= 1024 ? 8 : 4;
+    int rb = p.N <= 1024 ? 8 : 4;  // (8 rows at N = 1536 measured slower: one CTA per SM)
     if (const char* e = std::getenv("MNB_FFT_RB")) rb = std::max(1, std::min(rb, std::atoi(e)));  // tuning knob
     while (rb > 1 && rb * p.N / std::max(p.E, 1) > 512) rb >>= 1;
     return rb;
@@ -98,7 +98,7 @@ struct EventTimer {
 // all of them (out[(out_row0 + r) + f * ld_out]).  Scaled by n^{-1/2}.
 void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t rows, double2* tmp, int64_t ld_tmp,
               double2* out, int64_t ld_out, int64_t out_row0, bool select, const int32_t* sel, bool inverse,
-              double* ms_a, double* ms_b) {
+              double* ms_a, double* ms_b, const int32_t* fb_csr = nullptr) {
     FftPlan& P = ctx.fft_plan(n);
     const double scale = 1.0 / std::sqrt(double(n));
     auto rb = [&](const FftLenPlan& lp) { return rows == 1 ? 1 : rows_per_cta(lp); };
@@ -164,8 +164,13 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
         a.rows = rows;
         a.batches = P.n2;
         a.inverse = inverse;
+        a.num_sms = ctx.num_sms;
         EventTimer t(ctx, ms_b, 3);
-        run_fft(ctx, P.B, a);
+        // sketch: only the sampled frequencies are kept -> pruned pass B when the shape allows
+        const bool pruned = select && fb_csr && rows > 1 && !P.B.direct &&
+                            launch_fft_select_pruned(a, fb_csr, fb_csr + P.n2 + 1, ctx.num_sms, ctx.stream);
+        if (pruned) ctx.launches += 1;
+        else run_fft(ctx, P.B, a);
         t.stop();
     }
 }
@@ -464,8 +469,9 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
                              op.fb_n2 == FP.n2 ? op.fb_csr.as<int32_t>() : nullptr,
                              kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
         else
-                    fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
-                 kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
+            fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
+                     kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr,
+                     op.fb_n2 == FP.n2 ? op.fb_csr.as<int32_t>() : nullptr);
         if (op.ndups) {
             launch_copy_dups(out, ldo, out_row0 + s0, rs, op.dups.as<int32_t>(), op.ndups, ctx.stream);
             ctx.launches += 1;

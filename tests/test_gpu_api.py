@@ -1,0 +1,207 @@
+"""The reference's solver / least-squares contracts, run through the GPU path.
+
+Each test mirrors a TEST_CASE of /root/reference/proj/tests/test_solver.cpp or
+tests/test_lsq.cpp (cited per test): known answers, error behaviour (the
+exception types of include/minnorm/errors.hpp), determinism, reporting.
+Instances come from tests/instances.py (the BASELINE construction) or are
+written out as in the reference test.
+"""
+import numpy as np
+import pytest
+
+import paper_0905_4745_b200 as mn
+from oracle import minnorm_oracle as O
+from tests.instances import make_instance
+
+pytestmark = pytest.mark.gpu
+
+
+def crandn(rng, *shape):
+    return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) / np.sqrt(2)
+
+
+def conditioned_tall(n, m, kappa, seed):
+    """B = Q_n diag(sigma) Q_m^H, n x m, singular values log-spaced 1 -> 1/kappa."""
+    rng = np.random.default_rng(seed)
+    Qn, _ = np.linalg.qr(crandn(rng, n, m))
+    Qm, _ = np.linalg.qr(crandn(rng, m, m))
+    return (Qn * np.logspace(0, -np.log10(kappa), m)) @ Qm.conj().T
+
+
+# ------------------------------------------------------------ test_solver.cpp
+def test_orthonormal_row_analog(ctx):
+    """test_solver.cpp:45-63: 2 x 16 orthonormal rows force x = (1, 1, 0, ...)."""
+    A = np.zeros((2, 16), complex)
+    A[0, 0] = A[1, 1] = 1.0
+    b = np.array([1.0, 1.0], complex)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(epsilon=1e-8), ctx)
+    want = np.zeros(16, complex)
+    want[:2] = 1.0
+    assert np.linalg.norm(rep.x - want) <= 1e-8 * np.linalg.norm(want)
+    assert rep.residual_norm <= 1e-10
+    assert rep.lsq_converged
+
+
+def test_single_row_projects_onto_the_row(ctx):
+    """test_solver.cpp:65-75: A = (3, 4, 0, ...), b = 5 -> x = (0.6, 0.8, 0, ...)."""
+    A = np.zeros((1, 16), complex)
+    A[0, 0], A[0, 1] = 3.0, 4.0
+    b = np.array([5.0], complex)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(epsilon=1e-9), ctx)
+    want = np.zeros(16, complex)
+    want[0], want[1] = 0.6, 0.8
+    assert np.linalg.norm(rep.x - want) <= 1e-9
+
+
+def test_conditioned_instance_tracks_exact_solution(ctx):
+    """test_solver.cpp:77-90 (l = 16, eps = 1e-6, seed 73; healthy c_norm_ratio)."""
+    A, b = make_instance(4, 32, 1e3, seed=71)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(sketch_size=16, epsilon=1e-6, seed=73), ctx)
+    p = O.solve_svd(A, b)
+    assert np.linalg.norm(rep.x - p) <= 1e-6 * np.linalg.norm(p)
+    assert rep.lsq_converged
+    assert rep.c_norm_ratio <= 1.5
+
+
+def test_zero_rhs_short_circuits(ctx):
+    """test_solver.cpp:118-128 (src/solver.cpp:68-73)."""
+    A, _ = make_instance(3, 48, 1e2, seed=95)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, np.zeros(3, complex)), mn.SolverConfig(), ctx)
+    assert np.linalg.norm(rep.x) == 0.0
+    assert rep.residual_norm == 0.0
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(sketch_size=4), dict(sketch_size=12),
+                                dict(sketch_size=8, epsilon=2.0), dict(sketch_size=8, alpha=1.0)])
+def test_bad_configuration_raises_config_error(ctx, kw):
+    """test_solver.cpp:130-145: l outside (m, n), eps outside (0, 1), alpha <= 1."""
+    A, b = make_instance(4, 12, 1e1, seed=97)
+    with pytest.raises(mn.ConfigError):
+        mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(**kw), ctx)
+
+
+def test_dimension_and_finiteness_preconditions(ctx):
+    """test_solver.cpp:147-160 and ProblemInstance::validate (src/solver.cpp:37-48)."""
+    rng = np.random.default_rng(99)
+    with pytest.raises(mn.DimensionError):  # not underdetermined
+        mn.solve_randomized(mn.ProblemInstance(crandn(rng, 4, 4), crandn(rng, 4)), mn.SolverConfig(), ctx)
+    with pytest.raises(mn.DimensionError):  # b length
+        mn.solve_randomized(mn.ProblemInstance(crandn(rng, 2, 8), crandn(rng, 3)), mn.SolverConfig(), ctx)
+    bad = crandn(rng, 2, 64)
+    bad[1, 3] = np.nan
+    with pytest.raises(mn.DimensionError):  # non-finite A (checked on the device while sketching)
+        mn.solve_randomized(mn.ProblemInstance(bad, crandn(rng, 2)), mn.SolverConfig(), ctx)
+    with pytest.raises(mn.DimensionError):  # non-finite b
+        b = crandn(rng, 2)
+        b[0] = np.inf
+        mn.solve_randomized(mn.ProblemInstance(crandn(rng, 2, 64), b), mn.SolverConfig(), ctx)
+
+
+def test_rank_deficiency_is_reported(ctx):
+    """test_solver.cpp:162-174: a rank-1 2 x 16 matrix."""
+    rng = np.random.default_rng(101)
+    A = np.zeros((2, 16), complex)
+    A[0] = crandn(rng, 16)
+    A[1] = 2.0 * A[0]
+    b = np.array([1.0, 2.0], complex)
+    with pytest.raises(mn.RankDeficiencyError) as ei:
+        mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(sketch_size=8), ctx)
+    assert ei.value.deficient_columns() >= 1
+
+
+def test_unconverged_subsolver_is_reported_not_thrown(ctx):
+    """test_solver.cpp:176-185: lsq_max_iterations = 1."""
+    A, b = make_instance(6, 96, 1e5, seed=103)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(epsilon=1e-9, lsq_max_iterations=1), ctx)
+    assert not rep.lsq_converged
+    assert np.all(np.isfinite(rep.x))
+
+
+def test_fixed_seed_is_bitwise_reproducible_and_captures_c(ctx):
+    """test_solver.cpp:187-204: same bits of x and c across runs; A c = b; c only on request."""
+    A, b = make_instance(4, 64, 1e3, seed=105)
+    cfg = mn.SolverConfig(seed=107, capture_c=True)
+    r1 = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    r2 = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    assert r1.x.tobytes() == r2.x.tobytes()
+    assert r1.c is not None and r1.c.size == A.shape[1]
+    assert r1.c.tobytes() == r2.c.tobytes()
+    assert np.linalg.norm(A @ r1.c - b) <= 1e-10 * 1e3 * np.linalg.norm(b)
+    cfg.capture_c = False
+    assert mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx).c is None
+
+
+def test_report_fields(ctx):
+    """test_solver.cpp:206-213: step timings, sketch size, lsq_tau = eps^2 l / (alpha n)."""
+    A, b = make_instance(4, 64, 1e2, seed=109)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(), ctx)
+    assert all(t >= 0.0 for t in rep.step_seconds)
+    assert rep.sketch_size == 16
+    assert rep.lsq_tau == pytest.approx(1e-12 * 16.0 / (4.0 * 64.0))
+
+
+def test_with_replacement_sampling_solve(ctx):
+    """RandomStream::Sampling::with_replacement through the whole solve (dup > 1 in the stop rule)."""
+    A, b = make_instance(16, 256, 1e2, seed=111)
+    cfg = mn.SolverConfig(epsilon=1e-10, sampling=mn.Sampling.with_replacement)
+    rep = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx)
+    ref = O.solve_randomized(A, b, epsilon=1e-10, without=False)
+    p = O.solve_classical(A, b)
+    assert np.linalg.norm(rep.x - p) <= 1e-8 * np.linalg.norm(p)
+    assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
+
+
+# --------------------------------------------------------------- test_lsq.cpp
+def lsq(B, c, l, tau, seed, ctx, max_iterations=300):
+    return mn.solve_least_squares(B, c, mn.LsqConfig(sketch_size=l, tau=tau, stream_seed=seed,
+                                                     max_iterations=max_iterations), ctx)
+
+
+def test_lsq_orthonormal_columns_reduce_to_adjoint_projection(ctx):
+    """test_lsq.cpp:42-50."""
+    rng = np.random.default_rng(303)
+    B, _ = np.linalg.qr(crandn(rng, 64, 6))
+    c = crandn(rng, 64)
+    sol = lsq(B, c, 24, 1e-14, 45, ctx)
+    assert np.linalg.norm(sol.y - B.conj().T @ c) <= 1e-10 * np.linalg.norm(c)
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_lsq_excess_below_tau(ctx, trial):
+    """test_lsq.cpp:52-82: got - best <= tau best across conditions and tolerances."""
+    rng = np.random.default_rng(400 + trial)
+    m = 2 + trial
+    n = 16 * m
+    kappa = 10.0 ** (trial % 7)
+    B = conditioned_tall(n, m, kappa, 500 + trial)
+    c = B @ crandn(rng, m) + 0.25 * crandn(rng, n)
+    c /= np.linalg.norm(c)
+    tau = 10.0 ** (-4.0 - 4.0 * (trial % 3))
+    sol = lsq(B, c, 4 * m, tau, 600 + trial, ctx)
+    y_best = np.linalg.lstsq(B, c, rcond=None)[0]
+    best = np.linalg.norm(B @ y_best - c) ** 2
+    got = np.linalg.norm(B @ sol.y - c) ** 2
+    assert got - best <= tau * best + 1e-24
+    ref = O.solve_least_squares(np.asfortranarray(B.conj().T), c, 4 * m, tau, stream_seed=600 + trial)
+    assert abs(sol.iterations - ref.iterations) <= 1
+
+
+def test_lsq_residual_norms_never_increase(ctx):
+    """test_lsq.cpp:84-92."""
+    rng = np.random.default_rng(307)
+    B = conditioned_tall(128, 12, 1e4, 51)
+    c = B @ crandn(rng, 12) + 0.5 * crandn(rng, 128)
+    sol = lsq(B, c, 48, 1e-14, 53, ctx)
+    assert len(sol.residual_norms) >= 2
+    for k in range(1, len(sol.residual_norms)):
+        assert sol.residual_norms[k] <= sol.residual_norms[k - 1] * (1.0 + 1e-12)
+
+
+def test_lsq_fixed_seed_is_bitwise_reproducible(ctx):
+    """test_lsq.cpp:94-100."""
+    rng = np.random.default_rng(309)
+    B = conditioned_tall(80, 6, 1e2, 55)
+    c = crandn(rng, 80)
+    y1 = lsq(B, c, 24, 1e-10, 57, ctx).y
+    y2 = lsq(B, c, 24, 1e-10, 57, ctx).y
+    assert y1.tobytes() == y2.tobytes()

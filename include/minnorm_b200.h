@@ -39,6 +39,8 @@ extern "C" {
 #define MNB_F64 1  /* double (real A; config 5) */
 #define MNB_HOST 0
 #define MNB_DEVICE 1
+#define MNB_HOST_ASYNC 2 /* mnb_set_matrix: pinned host A, copied by the next solve in row slabs that
+                            overlap its sketches (caller keeps A alive until that call returns) */
 #define MNB_WITHOUT_REPLACEMENT 0 /* RandomStream::Sampling (rng.hpp:18) */
 #define MNB_WITH_REPLACEMENT 1
 
@@ -67,7 +69,10 @@ int mnb_shard_columns(int64_t n, int world_size, int rank, int64_t* col_begin, i
 /* The problem matrix A (ProblemInstance::A, include/minnorm/solver.hpp:14-24):
  * this rank's column shard A[:, col_begin : col_begin+n_local], column-major
  * with leading dimension lda >= m.  location MNB_DEVICE borrows the pointer
- * (caller keeps it alive; requires lda == m), MNB_HOST copies it to the GPU. */
+ * (caller keeps it alive; requires lda == m), MNB_HOST copies it to the GPU,
+ * MNB_HOST_ASYNC (single GPU, page-locked host memory; otherwise as MNB_HOST)
+ * defers the copy: mnb_solve_randomized streams A in row slabs and sketches
+ * each slab as it lands, and any other call first completes the copy. */
 int mnb_set_matrix(mnb_context* ctx, int dtype, int64_t m, int64_t n_global, int64_t col_begin,
                    int64_t n_local, const void* A, int64_t lda, int location);
 

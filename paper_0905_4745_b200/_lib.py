@@ -27,6 +27,7 @@ MNB_C128 = 0
 MNB_F64 = 1
 MNB_HOST = 0
 MNB_DEVICE = 1
+MNB_HOST_ASYNC = 2
 
 FIELDS = {"d": 0, "zeta": 1, "zeta_tilde": 2, "theta": 3, "theta_tilde": 4, "cos_theta": 5, "sin_theta": 6,
           "cos_theta_tilde": 7, "sin_theta_tilde": 8, "perm": 9, "perm_tilde": 10, "sample": 11}

@@ -149,11 +149,13 @@ class Context:
     def set_stream(self, stream_ptr: int) -> None:
         _check(self._lib.mnb_context_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
 
-    def set_matrix(self, A, n_global: Optional[int] = None, col_begin: int = 0) -> None:
+    def set_matrix(self, A, n_global: Optional[int] = None, col_begin: int = 0, deferred: bool = False) -> None:
         """A: this rank's column shard (m x n_local), complex128 or float64.
         numpy arrays are copied to the GPU; CUDA torch tensors are borrowed
         (column-major, i.e. a transposed-contiguous tensor or a (n,m) row-major
-        tensor viewed as A^T)."""
+        tensor viewed as A^T).  deferred=True (MNB_HOST_ASYNC): a page-locked
+        host array is copied by the next solve, overlapped with its sketches;
+        the array is kept referenced until that solve returns."""
         if _is_torch_cuda(A):
             import torch
             if A.dtype == torch.complex128:
@@ -177,7 +179,7 @@ class Context:
             A = np.asfortranarray(A)
             m, nl = A.shape
             self._keep = A
-            ptr, loc = _ptr(A), L.MNB_HOST
+            ptr, loc = _ptr(A), (L.MNB_HOST_ASYNC if deferred else L.MNB_HOST)
         n_global = nl if n_global is None else n_global
         _check(self._lib.mnb_set_matrix(self._h, dtype, m, n_global, col_begin, nl, ptr, m, loc))
         if loc == L.MNB_HOST:
@@ -293,7 +295,7 @@ def solve_randomized(inst: ProblemInstance, cfg: SolverConfig = SolverConfig(), 
             if A.shape[0] < 1 or A.shape[0] >= A.shape[1]:
                 raise DimensionError(f"problem must be underdetermined: 1 <= m < n, got m={A.shape[0]}, "
                                      f"n={A.shape[1]}")
-            ctx.set_matrix(A)
+            ctx.set_matrix(A, deferred=True)  # pinned host A: copied in slabs under the sketches
         else:
             ctx.set_matrix(A, n_global=ctx.n, col_begin=ctx.col_begin)
     b = _host_c128(inst.b.cpu().numpy() if _is_torch_cuda(inst.b) else inst.b)
@@ -307,8 +309,12 @@ def solve_randomized(inst: ProblemInstance, cfg: SolverConfig = SolverConfig(), 
         x = np.zeros(ctx.n_local, np.complex128)
         c = np.zeros(ctx.n_local, np.complex128) if cfg.capture_c else None
         xp, xl, cp = _ptr(x), L.MNB_HOST, (_ptr(c) if c is not None else None)
-    _check(ctx._lib.mnb_solve_randomized(ctx._h, _ptr(b), L.MNB_HOST, ctypes.byref(cfg._c()), xp, xl, cp,
-                                         ctypes.byref(rc)))
+    try:
+        _check(ctx._lib.mnb_solve_randomized(ctx._h, _ptr(b), L.MNB_HOST, ctypes.byref(cfg._c()), xp, xl, cp,
+                                             ctypes.byref(rc)))
+    finally:
+        if A is not None and not _is_torch_cuda(A):
+            ctx._keep = None  # a deferred host copy is complete once the solve returns
     return _report(rc, x, c)
 
 

@@ -173,6 +173,20 @@ int mnb_set_matrix(mnb_context* ctx, int dtype, int64_t m, int64_t n_global, int
         }
         const size_t out_esz = c.esz();
         void* dst = c.A_own.ensure(std::max<size_t>(size_t(m) * size_t(n_local) * out_esz, 16));
+        c.pending_host = false;
+        c.A_host = nullptr;
+        if (location == MNB_HOST_ASYNC && c.world == 1 && !promote && n_local > 0) {
+            cudaPointerAttributes attr{};
+            const bool pinned = cudaPointerGetAttributes(&attr, A) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+            cudaGetLastError();
+            if (pinned) {
+                c.A = dst;
+                c.A_host = A;
+                c.host_lda = lda;
+                c.pending_host = true;
+                return;
+            }
+        }
         const auto kind = location == MNB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         if (!promote) {
             MNB_CUDA(cudaMemcpy2DAsync(dst, size_t(m) * esz, A, size_t(lda) * esz, size_t(m) * esz, size_t(n_local), kind,
@@ -230,6 +244,7 @@ int mnb_solve_least_squares(mnb_context* ctx, const void* cvec, int c_location, 
     return guard([&] {
         auto& c = ctx->ctx;
         MNB_CUDA(cudaSetDevice(c.device));
+        ctx->ctx.make_resident();
         const double2* c_dev = static_cast<const double2*>(cvec);
         if (c_location != MNB_DEVICE) {
             double2* d = static_cast<double2*>(c.vec_n[2].ensure(size_t(std::max<int64_t>(c.n_local, 1)) * 16));
@@ -365,6 +380,7 @@ int mnb_srft_apply_to_columns(mnb_context* ctx, const mnb_srft* op, void* out, i
     return guard([&] {
         auto& c = ctx->ctx;
         MNB_CUDA(cudaSetDevice(c.device));
+        ctx->ctx.make_resident();
         mnb::require(c.A != nullptr || c.n_local == 0, MNB_ERR_INVALID_ARGUMENT, "no problem matrix set");
         mnb::require(op->host.n == c.n_global, MNB_ERR_INVALID_ARGUMENT, "apply_to_columns: matrix must have n rows");
         mnb::SrftDev& dev = c.op_dev[2];
@@ -395,6 +411,7 @@ int mnb_dft(mnb_context* ctx, int64_t n, void* x, int inverse) {
 int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch) {
     return guard([&] {
         MNB_CUDA(cudaSetDevice(ctx->ctx.device));
+        ctx->ctx.make_resident();
         *ms_per_launch = mnb::bench_pcg_pass(ctx->ctx, std::max(1, reps));
     });
 }

@@ -100,6 +100,11 @@ struct Context {
     int64_t m = 0, n_global = 0, col_begin = 0, n_local = 0;
     const void* A = nullptr;
     DevBuf A_own;
+    // deferred host copy (MNB_HOST_ASYNC): A_own is allocated, the bytes are still on the host
+    const void* A_host = nullptr;
+    int64_t host_lda = 0;
+    bool pending_host = false;
+    cudaStream_t copy_stream = nullptr;
 
     std::map<int64_t, std::unique_ptr<FftPlan>> fft_plans;
     int64_t launches = 0;  // own kernels launched (for reporting)
@@ -121,6 +126,7 @@ struct Context {
     cudaEvent_t event(size_t i);
     FftPlan& fft_plan(int64_t n);
     size_t esz() const { return dtype == MNB_F64 ? 8 : 16; }
+    void make_resident();  // completes a deferred host copy of A (synchronous)
 };
 
 // ---- SRFT on the GPU (srft_gpu.cu) ----

@@ -133,6 +133,17 @@ Context::~Context() {
     if (cublas) cublasDestroy(cublas);
     if (comm) ncclCommDestroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+void Context::make_resident() {
+    if (!pending_host) return;
+    const size_t e = esz();
+    MNB_CUDA(cudaMemcpy2DAsync(A_own.p, size_t(m) * e, A_host, size_t(host_lda) * e, size_t(m) * e, size_t(n_local),
+                               cudaMemcpyHostToDevice, stream));
+    MNB_CUDA(cudaStreamSynchronize(stream));
+    pending_host = false;
+    A_host = nullptr;
 }
 
 cudaEvent_t Context::event(size_t i) {
@@ -351,14 +362,14 @@ bool cholqr2_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R)
 }
 
 SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, DevBuf& Rbuf, double* kernel_ms,
-                       double* sketch_s, double* qr_s, double* redistribute_s) {
+                       double* sketch_s, double* qr_s, double* redistribute_s, bool presketched = false) {
     const int64_t l = op.host->l, m = ctx.m;
     double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
     double2* tau = dev<double2>(taubuf, size_t(m));
     double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
     cudaEvent_t e0 = ctx.event(12), e1 = ctx.event(13), e2 = ctx.event(14);
     MNB_CUDA(cudaEventRecord(e0, ctx.stream));
-    sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
+    if (!presketched) sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
     SketchQr out{S, tau, R, m, false};
     if (!(ctx.cholqr && cholqr2_r(ctx, S, l, m, R))) {
@@ -414,6 +425,18 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.world_size = ctx.world;
     rep.lsq_converged = 1;
     const int64_t launches0 = ctx.launches;
+    // a deferred host copy never outlives this call (the caller may release its buffer on return)
+    struct ResidentGuard {
+        Context& c;
+        ~ResidentGuard() {
+            if (c.pending_host) {
+                try {
+                    c.make_resident();
+                } catch (...) {
+                }
+            }
+        }
+    } resident_guard{ctx};
     if (b_zero) {  // src/solver.cpp:68-73
         if (ctx.n_local) {
             MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(ctx.n_local) * 16, ctx.stream));
@@ -427,32 +450,92 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const RandomStream root(cfg.seed);
     const uint64_t seed_T = root.derive_seed(11), seed_Tp = root.derive_seed(12);  // src/solver.cpp:19
     const int hw = int(std::max(2u, std::thread::hardware_concurrency()));
-    // T (needed first) is drawn with every host thread; T' is drawn in the
-    // background with half of them while this thread drives Steps 1-3 on the GPU.
+    // Deferred host A (MNB_HOST_ASYNC, one GPU): copy it in row slabs on a side stream now; both
+    // sketches then run slab by slab as the rows land, so the H2D hides the parameter draws, the
+    // sketches and most of Step 1.  Otherwise A is already resident.
+    const bool pipelined = ctx.pending_host && ctx.world == 1 && ctx.n_local > 0;
+    std::vector<std::pair<int64_t, int64_t>> slabs;  // (row0, rows)
+    if (!pipelined) ctx.make_resident();
+    // T (needed first) is drawn with every host thread; T' is drawn in the background with half
+    // of them while this thread drives Steps 1-3 on the GPU.  Pipelined: the first row slab of A
+    // goes out first, both operators are drawn while it is in flight, their (small) uploads queue
+    // behind it on the copy engine, then the remaining slabs follow.
     SrftHost T, Tp;
     auto noop = [](unsigned char*) {};
     double t_param_T = 0.0, t_param_Tp = 0.0;
-    const double tp0 = now_s();
-    build_srft_host(T, l, n, seed_T, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); },
-                    noop, hw);
-    t_param_T = now_s() - tp0;
-    auto fut_Tp = std::async(std::launch::async, [&] {
+    auto build_T = [&](int threads) {
+        const double s = now_s();
+        build_srft_host(T, l, n, seed_T, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); },
+                        noop, threads);
+        t_param_T = now_s() - s;
+    };
+    auto build_Tp = [&](int threads) {
         const double s = now_s();
         build_srft_host(Tp, l, n, seed_Tp, sampling, [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); },
-                        noop, std::max(1, hw / 2));
+                        noop, threads);
         t_param_Tp = now_s() - s;
-    });
+    };
+    std::future<void> fut_Tp;
+    SrftDev& Td = ctx.op_dev[0];
+    SrftDev& Tpd = ctx.op_dev[1];
+    if (pipelined) {
+        if (!ctx.copy_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+        const int64_t per = std::max<int64_t>(64, ((m + 7) / 8 + 7) & ~int64_t(7));
+        for (int64_t r0 = 0; r0 < m; r0 += per) slabs.emplace_back(r0, std::min(per, m - r0));
+        const size_t e = ctx.esz();
+        auto issue = [&](size_t k) {
+            const auto [r0, rows] = slabs[k];
+            MNB_CUDA(cudaMemcpy2DAsync(static_cast<unsigned char*>(ctx.A_own.p) + size_t(r0) * e, size_t(m) * e,
+                                       static_cast<const unsigned char*>(ctx.A_host) + size_t(r0) * e,
+                                       size_t(ctx.host_lda) * e, size_t(rows) * e, size_t(ctx.n_local),
+                                       cudaMemcpyHostToDevice, ctx.copy_stream));
+            MNB_CUDA(cudaEventRecord(ctx.event(200 + k), ctx.copy_stream));
+        };
+        issue(0);
+        const double tp0 = now_s();
+        auto f1 = std::async(std::launch::async, build_T, std::max(1, hw / 2));
+        build_Tp(std::max(1, hw - hw / 2));
+        f1.get();
+        (void)tp0;
+        upload_srft(ctx, T, Td);
+        upload_srft(ctx, Tp, Tpd);
+        for (size_t k = 1; k < slabs.size(); ++k) issue(k);
+    } else {
+        build_T(hw);
+        fut_Tp = std::async(std::launch::async, build_Tp, std::max(1, hw / 2));
+    }
 
     // ---- Step 1: S = T A^*
     double t0 = now_s();
-    SrftDev& Td = ctx.op_dev[0];
-    upload_srft(ctx, T, Td);
+    if (!pipelined) upload_srft(ctx, T, Td);
     int* nonfinite = dev<int>(ctx.flag, 1);
     MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx.stream));
-    ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
     double qr_s = 0.0, sk_s = 0.0;
+    if (pipelined) {
+        double2* S = dev<double2>(ctx.sk_S, size_t(l) * size_t(m));
+        double2* E = dev<double2>(ctx.sk_E, size_t(l) * size_t(m));
+        cudaEvent_t ea = ctx.event(198), eb = ctx.event(199);
+        MNB_CUDA(cudaEventRecord(ea, ctx.stream));
+        for (size_t k = 0; k < slabs.size(); ++k) {
+            const auto [r0, rows] = slabs[k];
+            MNB_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.event(200 + k), 0));
+            ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
+            sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, S, l, r0, rep.sketch_kernel_ms);
+            ctx.nonfinite = nullptr;
+            sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, E, l, r0, rep.sketch_kernel_ms);
+        }
+        MNB_CUDA(cudaEventRecord(eb, ctx.stream));
+        MNB_CUDA(cudaEventSynchronize(eb));
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
+        rep.sketch_seconds[0] = ms * 1e-3;  // both sketches, interleaved with the H2D
+        ctx.pending_host = false;
+        ctx.A_host = nullptr;
+    } else {
+        ctx.nonfinite = nonfinite;
+    }
     SketchQr sq = sketch_and_qr(ctx, Td, ctx.sk_S, ctx.tau_S, ctx.R_S, rep.sketch_kernel_ms, &sk_s, &qr_s,
-                                &rep.redistribute_seconds);
+                                &rep.redistribute_seconds, pipelined);
     ctx.nonfinite = nullptr;
     {
         int flag = 0;
@@ -466,7 +549,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         }
         if (flag) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
     }
-    rep.sketch_seconds[0] = sk_s;
+    if (!pipelined) rep.sketch_seconds[0] = sk_s;
     rep.qr_seconds[0] = qr_s;
     rep.step_seconds[0] = now_s() - t0;
 
@@ -529,15 +612,16 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
 
     // ---- Step 4: y = argmin ||A^* y - c||  (src/solver.cpp:104-114, src/lsq.cpp:43-113)
     t0 = now_s();
-    fut_Tp.get();
+    if (!pipelined) {
+        fut_Tp.get();
+        upload_srft(ctx, Tp, Tpd);
+    }
     rep.param_seconds = t_param_T + t_param_Tp;
-    SrftDev& Tpd = ctx.op_dev[1];
-    upload_srft(ctx, Tp, Tpd);
     sk_s = 0.0;
     qr_s = 0.0;
     SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, rep.sketch_kernel_ms, &sk_s, &qr_s,
-                                &rep.redistribute_seconds);
-    rep.sketch_seconds[1] = sk_s;
+                                &rep.redistribute_seconds, pipelined);
+    rep.sketch_seconds[1] = pipelined ? 0.0 : sk_s;
     rep.qr_seconds[1] = qr_s;
     if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
         throw Error(MNB_ERR_RANK_DEFICIENCY,

@@ -205,3 +205,25 @@ def test_lsq_fixed_seed_is_bitwise_reproducible(ctx):
     y1 = lsq(B, c, 24, 1e-10, 57, ctx).y
     y2 = lsq(B, c, 24, 1e-10, 57, ctx).y
     assert y1.tobytes() == y2.tobytes()
+
+
+def test_pinned_host_matrix_pipelined_copy_matches(ctx):
+    """A page-locked host A takes the MNB_HOST_ASYNC path (row-slab H2D overlapped with both
+    sketches); the solve must equal the one from a pageable (eagerly copied) A bit for bit."""
+    torch = pytest.importorskip("torch")
+    A, b = make_instance(192, 4096, 1e3, seed=113)
+    pinned = torch.empty((A.shape[1], A.shape[0]), dtype=torch.complex128, pin_memory=True)
+    pinned.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
+    A_pinned = pinned.numpy().T  # column-major view of page-locked memory
+    cfg = mn.SolverConfig(epsilon=1e-10, capture_c=True)
+    r_pin = mn.solve_randomized(mn.ProblemInstance(A_pinned, b), cfg, ctx)
+    r_page = mn.solve_randomized(mn.ProblemInstance(np.asfortranarray(A), b), cfg, ctx)
+    assert r_pin.x.tobytes() == r_page.x.tobytes()
+    assert r_pin.c.tobytes() == r_page.c.tobytes()
+    assert r_pin.lsq_iterations == r_page.lsq_iterations
+    # a later call on the same context sees the resident matrix
+    op = mn.build_srft(4 * 192, 4096, mn.derive_seed(42, 11))
+    ctx.set_matrix(A_pinned, deferred=True)
+    S1 = op.sketch(ctx)
+    ctx.set_matrix(np.asfortranarray(A))
+    assert np.array_equal(S1, op.sketch(ctx))

@@ -790,30 +790,9 @@ void launch_typed(const FftPassArgs& a, cudaStream_t stream) {
         // otherwise: the generic kernel below, addressing the blocked layout (half or quarter 8-row blocks)
     }
     dim3 grid(ceil_div(a.rows, Rb), unsigned(a.batches));
-    // Clusters of adjacent row blocks are co-scheduled, so the DRAM sees the
-    // neighbouring Rb*16-byte pieces of one index together (longer bursts).
-    int cl = 1;
-    if (const char* e = std::getenv("MNB_FFT_CLUSTER")) cl = std::max(1, std::atoi(e));
-    while (cl > 1 && grid.x % cl) cl >>= 1;
     auto kern = a.inverse ? fft_pass_kernel<Rb, E, true> : fft_pass_kernel<Rb, E, false>;
     MNB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    if (cl > 1) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = cl;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        MNB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
-    } else {
-        kern<<<grid, threads, smem, stream>>>(a);
-    }
+    kern<<<grid, threads, smem, stream>>>(a);
     MNB_LAUNCH_CHECK();
 }
 

@@ -49,7 +49,6 @@ bool fft_tile_fits(int N, int E) { return size_t(N) * 12 * 16 + 16 <= size_t(227
 
 int rows_per_cta(const FftLenPlan& p) {
     int rb = p.N <= 1024 ? 8 : 4;  // (8 rows at N = 1536 measured slower: one CTA per SM)
-    if (const char* e = std::getenv("MNB_FFT_RB")) rb = std::max(1, std::min(rb, std::atoi(e)));  // tuning knob
     while (rb > 1 && rb * p.N / std::max(p.E, 1) > 512) rb >>= 1;
     return rb;
 }

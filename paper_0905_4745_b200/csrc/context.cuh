@@ -120,10 +120,21 @@ struct Context {
     PinnedBuf pin_params[2], pin_small;
     SrftDev op_dev[3];  // device copies of the operators: [0] T, [1] T', [2] standalone SRFT calls (grow-only)
     std::vector<cudaEvent_t> events;
+    // deferred kernel timers (EventTimer): event pool + pending (start, stop, accumulator)
+    struct PendingTimer {
+        cudaEvent_t a, b;
+        double* acc;
+    };
+    std::vector<cudaEvent_t> timer_pool;
+    size_t timer_next = 0;
+    std::vector<PendingTimer> timers;
+    cudaStream_t aux_stream = nullptr;  // second compute stream (QRs / Steps 2-3 beside the sketches and passes)
     std::vector<unsigned char> host_work;  // cuSOLVER host workspace (kept alive across async calls)
 
     ~Context();
     cudaEvent_t event(size_t i);
+    cudaEvent_t timer_event();
+    void resolve_timers();  // synchronizes on the pending timers and accumulates them
     FftPlan& fft_plan(int64_t n);
     size_t esz() const { return dtype == MNB_F64 ? 8 : 16; }
     void make_resident();  // completes a deferred host copy of A (synchronous)

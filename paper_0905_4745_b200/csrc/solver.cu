@@ -128,6 +128,8 @@ void sync(Context& ctx) { MNB_CUDA(cudaStreamSynchronize(ctx.stream)); }
 
 Context::~Context() {
     for (auto e : events) if (e) cudaEventDestroy(e);
+    for (auto e : timer_pool) if (e) cudaEventDestroy(e);
+    if (aux_stream) cudaStreamDestroy(aux_stream);
     if (cusolver_params) cusolverDnDestroyParams(cusolver_params);
     if (cusolver) cusolverDnDestroy(cusolver);
     if (cublas) cublasDestroy(cublas);
@@ -146,6 +148,26 @@ void Context::make_resident() {
     A_host = nullptr;
 }
 
+cudaEvent_t Context::timer_event() {
+    if (timer_next == timer_pool.size()) {
+        cudaEvent_t e;
+        MNB_CUDA(cudaEventCreate(&e));
+        timer_pool.push_back(e);
+    }
+    return timer_pool[timer_next++];
+}
+
+void Context::resolve_timers() {
+    for (const auto& t : timers) {
+        MNB_CUDA(cudaEventSynchronize(t.b));
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, t.a, t.b));
+        *t.acc += ms;
+    }
+    timers.clear();
+    timer_next = 0;
+}
+
 cudaEvent_t Context::event(size_t i) {
     while (events.size() <= i) {
         cudaEvent_t e;
@@ -160,8 +182,20 @@ cudaEvent_t Context::event(size_t i) {
 // c: this rank's n_local entries (device).  y: m entries (device).
 // x, ax (optional): also accumulate x = A^H y = sum_k alpha_k t_k (this rank's columns) and
 // A x = sum_k alpha_k s_k inside the CG passes, so Step 5 (src/solver.cpp:118-125) needs no extra pass.
+// The INIT pass of the CG (lsq.cpp:77-86: r = c, s = A c, ||c||^2) on ctx.stream.  It needs only c,
+// so the solve launches it ahead of the preconditioner's QR (run_cg with init_done).
+void launch_cg_init_pass(Context& ctx, const double2* c, double2* x) {
+    const int64_t n = ctx.n_local;
+    double2* r = dev<double2>(ctx.vec_n[0], size_t(std::max<int64_t>(n, 1)));
+    double2* t = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(n, 1)));
+    PassBuffers pb = pass_buffers(ctx);
+    MNB_CUDA(cudaEventRecord(ctx.event(20), ctx.stream));
+    fused_pass(ctx, pb, PCG_INIT, nullptr, c, t, r, nullptr, x);
+    MNB_CUDA(cudaEventRecord(ctx.event(21), ctx.stream));
+}
+
 LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
-                 double dup, double2* y, bool want_norms, double2* x, double2* ax) {
+                 double dup, double2* y, bool want_norms, double2* x, double2* ax, bool init_done) {
     const int64_t m = ctx.m, n = ctx.n_local;
     LsqResult res;
     const double t0 = now_s();
@@ -200,9 +234,7 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     launch_init_state(st, tau, dup, (long long)max_it, ctx.stream);
     // initial state (lsq.cpp:77-86): r = c, g = M^H c, dir = g
     cudaEvent_t ea = ctx.event(20), eb = ctx.event(21);
-    MNB_CUDA(cudaEventRecord(ea, ctx.stream));
-    fused_pass(ctx, pb, PCG_INIT, nullptr, c, t, r, nullptr, x);
-    MNB_CUDA(cudaEventRecord(eb, ctx.stream));
+    if (!init_done) launch_cg_init_pass(ctx, c, x);
     launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 1, ctx.stream, ax);
     launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 1, ctx.stream);
     ctx.launches += 3;
@@ -361,15 +393,12 @@ bool cholqr2_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R)
     return true;
 }
 
-SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, DevBuf& Rbuf, double* kernel_ms,
-                       double* sketch_s, double* qr_s, double* redistribute_s, bool presketched = false) {
-    const int64_t l = op.host->l, m = ctx.m;
-    double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
+// QR of a finished l x m sketch on ctx.stream (CholeskyQR2, else Householder); qr_s += device time.
+SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBuf& Rbuf, double* qr_s) {
+    const int64_t m = ctx.m;
     double2* tau = dev<double2>(taubuf, size_t(m));
     double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
-    cudaEvent_t e0 = ctx.event(12), e1 = ctx.event(13), e2 = ctx.event(14);
-    MNB_CUDA(cudaEventRecord(e0, ctx.stream));
-    if (!presketched) sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
+    cudaEvent_t e1 = ctx.timer_event(), e2 = ctx.timer_event();
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
     SketchQr out{S, tau, R, m, false};
     if (!(ctx.cholqr && cholqr2_r(ctx, S, l, m, R))) {
@@ -380,13 +409,39 @@ SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& ta
     }
     MNB_CUDA(cudaEventRecord(e2, ctx.stream));
     MNB_CUDA(cudaEventSynchronize(e2));
-    float a = 0.f, b = 0.f;
-    MNB_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    float b = 0.f;
     MNB_CUDA(cudaEventElapsedTime(&b, e1, e2));
-    if (sketch_s) *sketch_s += a * 1e-3;
     if (qr_s) *qr_s += b * 1e-3;
     return out;
 }
+
+SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, DevBuf& Rbuf, double* kernel_ms,
+                       double* sketch_s, double* qr_s, double* redistribute_s) {
+    const int64_t l = op.host->l, m = ctx.m;
+    double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
+    cudaEvent_t e0 = ctx.timer_event(), e1 = ctx.timer_event();
+    MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+    sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
+    MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+    SketchQr out = qr_of_sketch(ctx, S, l, taubuf, Rbuf, qr_s);
+    float a = 0.f;
+    MNB_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    if (sketch_s) *sketch_s += a * 1e-3;
+    return out;
+}
+
+// Run a block of the solve on another stream: ctx.stream and the library handles follow.
+struct OnStream {
+    Context& c;
+    cudaStream_t saved;
+    OnStream(Context& ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) { bind(s); }
+    ~OnStream() { bind(saved); }
+    void bind(cudaStream_t s) {
+        c.stream = s;
+        cublasSetStream(c.cublas, s);
+        cusolverDnSetStream(c.cusolver, s);
+    }
+};
 
 unsigned char* pinned_alloc(PinnedBuf& pb, size_t bytes) { return static_cast<unsigned char*>(pb.ensure(bytes)); }
 
@@ -394,10 +449,54 @@ void validate_matrix_set(const Context& ctx) {
     require(ctx.A != nullptr || ctx.n_local == 0, MNB_ERR_INVALID_ARGUMENT, "no problem matrix set (mnb_set_matrix)");
 }
 
+// Step 2 (src/solver.cpp:93-96): z = Q [R^{-H} b; 0] on ctx.stream.
+void step2_z(Context& ctx, const SketchQr& sq, const double2* b_host, int64_t l, int64_t m, double2* z) {
+    const auto* Rc = reinterpret_cast<const cuDoubleComplex*>(sq.R);
+    if (sq.householder) {
+        MNB_CUDA(cudaMemsetAsync(z, 0, size_t(l) * 16, ctx.stream));
+        MNB_CUDA(cudaMemcpyAsync(z, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
+                                 int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(z), 1),
+                     "ztrsv");
+        int lwork = 0;
+        cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
+                                                   reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
+                                                   reinterpret_cast<const cuDoubleComplex*>(sq.tau),
+                                                   reinterpret_cast<const cuDoubleComplex*>(z), int(l), &lwork),
+                       "unmqr_bufferSize");
+        auto* work = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
+        cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
+                                        reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
+                                        reinterpret_cast<const cuDoubleComplex*>(sq.tau),
+                                        reinterpret_cast<cuDoubleComplex*>(z), int(l), work, lwork,
+                                        dev<int>(ctx.qr_info, 1)),
+                       "unmqr");
+        return;
+    }
+    // CholeskyQR2: Q = S R^{-1} = Q1 R2^{-1}, so z = Q1 (R2^{-1} (R^{-H} b))
+    double2* w = dev<double2>(ctx.vec_m[6], size_t(m));
+    MNB_CUDA(cudaMemcpyAsync(w, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
+                             int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(w), 1),
+                 "ztrsv");
+    cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
+                             reinterpret_cast<const cuDoubleComplex*>(ctx.R2.p), int(m),
+                             reinterpret_cast<cuDoubleComplex*>(w), 1),
+                 "ztrsv");
+    const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0), czero = make_cuDoubleComplex(0.0, 0.0);
+    cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &cone,
+                             reinterpret_cast<const cuDoubleComplex*>(ctx.qwork.p), int(l),
+                             reinterpret_cast<const cuDoubleComplex*>(w), 1, &czero, reinterpret_cast<cuDoubleComplex*>(z),
+                             1),
+                 "zgemv");
+}
+
 // ---------------------------------------------------- solve_randomized ----
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep) {
     const double t_start = now_s();
+    ctx.timers.clear();  // drop timers of an aborted call (they point into its report)
+    ctx.timer_next = 0;
     validate_matrix_set(ctx);
     const int64_t m = ctx.m, n = ctx.n_global;
     // ProblemInstance::validate (src/solver.cpp:37-48); A's finiteness is checked on the device below.
@@ -505,132 +604,132 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         fut_Tp = std::async(std::launch::async, build_Tp, std::max(1, hw / 2));
     }
 
-    // ---- Step 1: S = T A^*
-    double t0 = now_s();
-    if (!pipelined) upload_srft(ctx, T, Td);
+    // Streams: the sketches and the CG passes (memory-bound) run on ctx.stream; with one GPU the
+    // QRs and Steps 2-3 (tensor-core / latency-bound) run on an auxiliary stream beside them:
+    //   s1: sketch S | sketch E | INIT pass (after c) | CG (after R')
+    //   s2:          | QR(S), Step 2, Step 3 (c)      | QR(E)
+    const bool concurrent = ctx.world == 1;
+    cudaStream_t s1 = ctx.stream;
+    if (concurrent && !ctx.aux_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
+    cudaStream_t s2 = concurrent ? ctx.aux_stream : s1;
     int* nonfinite = dev<int>(ctx.flag, 1);
-    MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), ctx.stream));
-    double qr_s = 0.0, sk_s = 0.0;
+    double2* Sbuf = dev<double2>(ctx.sk_S, size_t(l) * size_t(m));
+    double2* Ebuf = dev<double2>(ctx.sk_E, size_t(l) * size_t(m));
+    double qr_s0 = 0.0, qr_s1 = 0.0;
+    const double t_sol0 = now_s();
+    double t0 = t_sol0;
+
+    // ---- Step 1 (and Step 4's sketch): S = T A^*, E = T' A^*  (src/solver.cpp:80-81, src/lsq.cpp:55-56)
+    MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s1));
+    cudaEvent_t eA = ctx.timer_event(), eS = ctx.timer_event(), eE = ctx.timer_event();
+    MNB_CUDA(cudaEventRecord(eA, s1));
     if (pipelined) {
-        double2* S = dev<double2>(ctx.sk_S, size_t(l) * size_t(m));
-        double2* E = dev<double2>(ctx.sk_E, size_t(l) * size_t(m));
-        cudaEvent_t ea = ctx.event(198), eb = ctx.event(199);
-        MNB_CUDA(cudaEventRecord(ea, ctx.stream));
         for (size_t k = 0; k < slabs.size(); ++k) {
             const auto [r0, rows] = slabs[k];
-            MNB_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.event(200 + k), 0));
+            MNB_CUDA(cudaStreamWaitEvent(s1, ctx.event(200 + k), 0));
             ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
-            sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, S, l, r0, rep.sketch_kernel_ms);
+            sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Sbuf, l, r0, rep.sketch_kernel_ms);
             ctx.nonfinite = nullptr;
-            sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, E, l, r0, rep.sketch_kernel_ms);
+            sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Ebuf, l, r0, rep.sketch_kernel_ms);
         }
-        MNB_CUDA(cudaEventRecord(eb, ctx.stream));
-        MNB_CUDA(cudaEventSynchronize(eb));
-        float ms = 0.f;
-        MNB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
-        rep.sketch_seconds[0] = ms * 1e-3;  // both sketches, interleaved with the H2D
+        MNB_CUDA(cudaEventRecord(eS, s1));
+        MNB_CUDA(cudaEventRecord(eE, s1));
         ctx.pending_host = false;
         ctx.A_host = nullptr;
     } else {
+        upload_srft(ctx, T, Td);
         ctx.nonfinite = nonfinite;
+        sketch_matrix(ctx, Td, Sbuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+        ctx.nonfinite = nullptr;
+        MNB_CUDA(cudaEventRecord(eS, s1));
+        if (concurrent) {  // E's sketch queues behind S's on s1 while s2 factors S
+            fut_Tp.get();
+            upload_srft(ctx, Tp, Tpd);
+            sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+            MNB_CUDA(cudaEventRecord(eE, s1));
+        }
     }
-    SketchQr sq = sketch_and_qr(ctx, Td, ctx.sk_S, ctx.tau_S, ctx.R_S, rep.sketch_kernel_ms, &sk_s, &qr_s,
-                                &rep.redistribute_seconds, pipelined);
-    ctx.nonfinite = nullptr;
+
+    // ---- Step 1 QR and Steps 2-3 on s2
+    SketchQr sq;
+    double2* c_vec = dev<double2>(ctx.vec_n[2], size_t(n));
+    double2* z = dev<double2>(ctx.rhs, size_t(l));
+    cudaEvent_t eC = ctx.timer_event();
     {
-        int flag = 0;
+        OnStream on(ctx, s2);
+        MNB_CUDA(cudaStreamWaitEvent(s2, eS, 0));
+        sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0);
+        int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
         MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
         sync(ctx);
         if (ctx.world > 1) {
-            int* f = dev<int>(ctx.flag, 1);
-            nccl_check(ncclAllReduce(f, f, 1, ncclInt, ncclMax, ctx.comm, ctx.stream), "ncclAllReduce");
-            MNB_CUDA(cudaMemcpyAsync(&flag, f, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+            nccl_check(ncclAllReduce(nonfinite, nonfinite, 1, ncclInt, ncclMax, ctx.comm, ctx.stream), "ncclAllReduce");
+            MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
             sync(ctx);
         }
         if (flag) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
-    }
-    if (!pipelined) rep.sketch_seconds[0] = sk_s;
-    rep.qr_seconds[0] = qr_s;
-    rep.step_seconds[0] = now_s() - t0;
+        rep.step_seconds[0] = now_s() - t0;
 
-    // ---- Step 2: z = Q [R^{-H} b; 0]  (src/solver.cpp:85-97)
-    t0 = now_s();
-    if (int64_t bad = deficient_count(ctx, sq.R, sq.ldR, m, l); bad > 0)
-        throw Error(MNB_ERR_RANK_DEFICIENCY,
-                    "sketch S = T A* lost rank (" + std::to_string(bad) +
-                        " dependent columns); the problem matrix is rank deficient",
-                    bad);
-    double2* z = dev<double2>(ctx.rhs, size_t(l));
-    const auto* Rc = reinterpret_cast<const cuDoubleComplex*>(sq.R);
-    if (sq.householder) {
-        MNB_CUDA(cudaMemsetAsync(z, 0, size_t(l) * 16, ctx.stream));
-        MNB_CUDA(cudaMemcpyAsync(z, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
-                                 int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(z), 1),
-                     "ztrsv");
-        int lwork = 0;
-        cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
-                                                   reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
-                                                   reinterpret_cast<const cuDoubleComplex*>(sq.tau),
-                                                   reinterpret_cast<const cuDoubleComplex*>(z), int(l), &lwork),
-                       "unmqr_bufferSize");
-        auto* work = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
-        cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(l), 1, int(m),
-                                        reinterpret_cast<const cuDoubleComplex*>(sq.S), int(l),
-                                        reinterpret_cast<const cuDoubleComplex*>(sq.tau),
-                                        reinterpret_cast<cuDoubleComplex*>(z), int(l), work, lwork,
-                                        dev<int>(ctx.qr_info, 1)),
-                       "unmqr");
-    } else {
-        // z = Q [R^{-H} b; 0] with Q = S R^{-1} = Q1 R2^{-1}:  z = Q1 (R2^{-1} (R^{-H} b))
-        double2* w = dev<double2>(ctx.vec_m[6], size_t(m));
-        MNB_CUDA(cudaMemcpyAsync(w, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), Rc,
-                                 int(sq.ldR), reinterpret_cast<cuDoubleComplex*>(w), 1),
-                     "ztrsv");
-        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
-                                 reinterpret_cast<const cuDoubleComplex*>(ctx.R2.p), int(m),
-                                 reinterpret_cast<cuDoubleComplex*>(w), 1),
-                     "ztrsv");
-        const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0), czero = make_cuDoubleComplex(0.0, 0.0);
-        cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &cone,
-                                 reinterpret_cast<const cuDoubleComplex*>(ctx.qwork.p), int(l),
-                                 reinterpret_cast<const cuDoubleComplex*>(w), 1, &czero,
-                                 reinterpret_cast<cuDoubleComplex*>(z), 1),
-                     "zgemv");
-    }
-    sync(ctx);
-    rep.step_seconds[1] = now_s() - t0;
+        // ---- Step 2: z = Q [R^{-H} b; 0]  (src/solver.cpp:85-97)
+        t0 = now_s();
+        if (int64_t bad = deficient_count(ctx, sq.R, sq.ldR, m, l); bad > 0)
+            throw Error(MNB_ERR_RANK_DEFICIENCY,
+                        "sketch S = T A* lost rank (" + std::to_string(bad) +
+                            " dependent columns); the problem matrix is rank deficient",
+                        bad);
+        step2_z(ctx, sq, b_host, l, m, z);
+        sync(ctx);
+        rep.step_seconds[1] = now_s() - t0;
 
-    // ---- Step 3: c = T^* z  (src/solver.cpp:100-102)
-    t0 = now_s();
-    double2* c_vec = dev<double2>(ctx.vec_n[2], size_t(n));
-    srft_adjoint_vec(ctx, Td, z, c_vec);
+        // ---- Step 3: c = T^* z  (src/solver.cpp:100-102)
+        t0 = now_s();
+        srft_adjoint_vec(ctx, Td, z, c_vec);
+        MNB_CUDA(cudaEventRecord(eC, ctx.stream));
+        sync(ctx);
+        rep.step_seconds[2] = now_s() - t0;
+    }
     const double2* c_loc = c_vec + ctx.col_begin;
-    sync(ctx);
-    rep.step_seconds[2] = now_s() - t0;
 
     // ---- Step 4: y = argmin ||A^* y - c||  (src/solver.cpp:104-114, src/lsq.cpp:43-113)
     t0 = now_s();
-    if (!pipelined) {
+    if (!concurrent) {
         fut_Tp.get();
         upload_srft(ctx, Tp, Tpd);
+        sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+        MNB_CUDA(cudaEventRecord(eE, s1));
     }
     rep.param_seconds = t_param_T + t_param_Tp;
-    sk_s = 0.0;
-    qr_s = 0.0;
-    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, rep.sketch_kernel_ms, &sk_s, &qr_s,
-                                &rep.redistribute_seconds, pipelined);
-    rep.sketch_seconds[1] = pipelined ? 0.0 : sk_s;
-    rep.qr_seconds[1] = qr_s;
-    if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
-        throw Error(MNB_ERR_RANK_DEFICIENCY,
-                    "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
-                    bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
     double2* ax = dev<double2>(ctx.vec_m[7], size_t(m));
+    double2* xacc = ctx.n_local ? x_dev : nullptr;
+    // the INIT pass (r = c, s = A c) needs only c: on s1 while s2 factors E
+    MNB_CUDA(cudaStreamWaitEvent(s1, eC, 0));
+    launch_cg_init_pass(ctx, c_loc, xacc);
+    SketchQr eq;
+    cudaEvent_t eQ = ctx.timer_event();
+    {
+        OnStream on(ctx, s2);
+        MNB_CUDA(cudaStreamWaitEvent(s2, eE, 0));
+        eq = qr_of_sketch(ctx, Ebuf, l, ctx.tau_E, ctx.R_E, &qr_s1);
+        if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
+            throw Error(MNB_ERR_RANK_DEFICIENCY,
+                        "solve_least_squares: sketch QR found " + std::to_string(bad) +
+                            " numerically dependent columns",
+                        bad);
+        MNB_CUDA(cudaEventRecord(eQ, ctx.stream));
+    }
+    MNB_CUDA(cudaStreamWaitEvent(s1, eQ, 0));
     LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false,
-                          ctx.n_local ? x_dev : nullptr, ax);
+                          xacc, ax, /*init_done=*/true);
+    {
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, eA, eS));
+        rep.sketch_seconds[0] = ms * 1e-3;
+        MNB_CUDA(cudaEventElapsedTime(&ms, eS, eE));
+        rep.sketch_seconds[1] = ms * 1e-3;  // pipelined: 0 (both sketches are interleaved in [0])
+    }
+    rep.qr_seconds[0] = qr_s0;
+    rep.qr_seconds[1] = qr_s1;
     rep.lsq_iterations = ls.iterations;
     rep.lsq_converged = ls.converged ? 1 : 0;
     rep.lsq_achieved_excess = ls.achieved_excess;
@@ -657,6 +756,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.residual_norm = std::sqrt(res2);
     const double xnorm = std::sqrt(ls.xx);
     rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
+    ctx.resolve_timers();
     rep.kernel_launches = ctx.launches - launches0;
     rep.total_seconds = now_s() - t_start;
 }
@@ -665,6 +765,8 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
                          double* residual_norms, mnb_lsq_solution& sol) {
     validate_matrix_set(ctx);
+    ctx.timers.clear();
+    ctx.timer_next = 0;
     const int64_t m = ctx.m, n = ctx.n_global;  // B = A^H is n x m
     // src/lsq.cpp:45-53
     if (m < 1 || n <= m) throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: B must be tall (n > m >= 1)");
@@ -685,7 +787,7 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
     LsqResult ls = run_cg(ctx, c_dev, eq.R, eq.ldR, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
-                          residual_norms != nullptr, nullptr, nullptr);
+                          residual_norms != nullptr, nullptr, nullptr, false);
     MNB_CUDA(cudaMemcpyAsync(y_host, y, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
     sync(ctx);
     sol.achieved_excess = ls.achieved_excess;

@@ -69,24 +69,24 @@ void run_fft(Context& ctx, const FftLenPlan& p, FftPassArgs a) {
     ctx.launches += 1;
 }
 
+// Kernel timing without host syncs: the event pair is resolved (summed into
+// *acc) by Context::resolve_timers() at the end of the solve, so launches
+// queue back to back and other streams can overlap them.
 struct EventTimer {
     Context& ctx;
     double* acc;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    EventTimer(Context& c, double* a, size_t slot) : ctx(c), acc(a) {
+    cudaEvent_t e0 = nullptr;
+    EventTimer(Context& c, double* a, size_t /*slot*/) : ctx(c), acc(a) {
         if (acc) {
-            e0 = ctx.event(2 * slot);
-            e1 = ctx.event(2 * slot + 1);
+            e0 = ctx.timer_event();
             MNB_CUDA(cudaEventRecord(e0, ctx.stream));
         }
     }
     void stop() {
         if (acc) {
+            cudaEvent_t e1 = ctx.timer_event();
             MNB_CUDA(cudaEventRecord(e1, ctx.stream));
-            MNB_CUDA(cudaEventSynchronize(e1));
-            float ms = 0.f;
-            MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            *acc += ms;
+            ctx.timers.push_back({e0, e1, acc});
         }
     }
 };

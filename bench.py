@@ -92,9 +92,44 @@ def make_b(cfg):
 
 # ---------------------------------------------------------------- clocks ---
 class ClockSampler:
+    """SM clock / throttle-reason samples during the timed region.  In-process
+    NVML polling (a light driver query every 100 ms; spawning nvidia-smi inside
+    the timed region stalls millisecond-scale solves); nvidia-smi as fallback."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown"}
+
     def __init__(self, device_index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
+        import threading
+        self.sm, self.mx, self.reasons = [], 0.0, set()
+        self.stop_flag = threading.Event()
+        self.thread = None
         self.proc = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            def run():
+                while True:
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, name in self.REASONS.items():
+                            if bits & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    if self.stop_flag.wait(0.1):
+                        return
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception:
+            self._start_smi(device_index)
+
+    def _start_smi(self, device_index):
+        self.path = tempfile.mktemp(suffix=".csv")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(device_index),
@@ -107,29 +142,31 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
-        if not self.proc:
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=5)
+        elif self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            with open(self.path) as f:
+                for line in f:
+                    p = [x.strip() for x in line.split(",")]
+                    if len(p) < 8:
+                        continue
+                    try:
+                        self.sm.append(float(p[0]))
+                        self.mx = max(self.mx, float(p[1]))
+                    except ValueError:
+                        continue
+                    for nm, v in zip(names, p[4:8]):
+                        if v.lower() == "active":
+                            self.reasons.add(nm)
+            os.unlink(self.path)
+        if not self.sm:
             return None
-        self.proc.terminate()
-        self.proc.wait(timeout=10)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        with open(self.path) as f:
-            for line in f:
-                p = [x.strip() for x in line.split(",")]
-                if len(p) < 8:
-                    continue
-                try:
-                    sm.append(float(p[0]))
-                    mx = max(mx, float(p[1]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, p[4:8]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-        os.unlink(self.path)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 # ----------------------------------------------------------- CPU baseline --

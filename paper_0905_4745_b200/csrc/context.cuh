@@ -166,6 +166,7 @@ struct LsqResult {
     double pcg_seconds = 0.0;
 };
 void sync(Context& ctx);
+void trace(const char* what);  // MNB_TRACE=1: host phase timestamps on stderr
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep);
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,

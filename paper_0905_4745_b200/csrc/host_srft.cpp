@@ -315,8 +315,8 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         }
     };
     {
-        // a worker per 64K indices is plenty (small operators are drawn in microseconds)
-        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, 1 + n / 65536)));
+        // one worker per 2K indices up to the pool size (thread start-up outweighs tiny operators)
+        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, n / 2048)));
         std::vector<std::thread> pool;
         for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
         worker();

@@ -12,6 +12,8 @@
 // (2m+4 doubles) per CG iteration; the sketch redistributes A with one
 // all-to-all (srft_gpu.cu).  The small m-space work is replicated per rank.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <future>
 #include <thread>
@@ -27,6 +29,7 @@ constexpr double kEps = 2.220446049250313080847e-16;
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+
 
 void cusolver_check(cusolverStatus_t s, const char* what) {
     if (s != CUSOLVER_STATUS_SUCCESS) throw Error(MNB_ERR_CUDA, std::string(what) + " failed (cusolver status " + std::to_string(int(s)) + ")");
@@ -123,6 +126,16 @@ void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w,
 }
 
 }  // namespace
+
+// MNB_TRACE=1: host timestamps of the solve's phases on stderr (diagnostics)
+void trace(const char* what) {
+    static const bool on = std::getenv("MNB_TRACE") != nullptr;
+    if (!on) return;
+    static thread_local double last = 0.0;
+    const double t = now_s();
+    std::fprintf(stderr, "[mnb] %-28s +%8.3f ms\n", what, last > 0.0 ? (t - last) * 1e3 : 0.0);
+    last = t;
+}
 
 void sync(Context& ctx) { MNB_CUDA(cudaStreamSynchronize(ctx.stream)); }
 
@@ -609,6 +622,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     //   s1: sketch S | sketch E | INIT pass (after c) | CG (after R')
     //   s2:          | QR(S), Step 2, Step 3 (c)      | QR(E)
     const bool concurrent = ctx.world == 1;
+    trace("params done");
     cudaStream_t s1 = ctx.stream;
     if (concurrent && !ctx.aux_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
     cudaStream_t s2 = concurrent ? ctx.aux_stream : s1;
@@ -639,16 +653,19 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     } else {
         upload_srft(ctx, T, Td);
         ctx.nonfinite = nonfinite;
+    trace("upload T");
         sketch_matrix(ctx, Td, Sbuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
         ctx.nonfinite = nullptr;
         MNB_CUDA(cudaEventRecord(eS, s1));
-        if (concurrent) {  // E's sketch queues behind S's on s1 while s2 factors S
+        if (concurrent) {    trace("sketch S issued");
+  // E's sketch queues behind S's on s1 while s2 factors S
             fut_Tp.get();
             upload_srft(ctx, Tp, Tpd);
             sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
             MNB_CUDA(cudaEventRecord(eE, s1));
         }
     }
+    trace("sketch E issued");
 
     // ---- Step 1 QR and Steps 2-3 on s2
     SketchQr sq;
@@ -659,6 +676,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         OnStream on(ctx, s2);
         MNB_CUDA(cudaStreamWaitEvent(s2, eS, 0));
         sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0);
+    trace("QR(S)");
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
         MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
         sync(ctx);
@@ -688,6 +706,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         sync(ctx);
         rep.step_seconds[2] = now_s() - t0;
     }
+    trace("steps 2-3");
     const double2* c_loc = c_vec + ctx.col_begin;
 
     // ---- Step 4: y = argmin ||A^* y - c||  (src/solver.cpp:104-114, src/lsq.cpp:43-113)
@@ -705,6 +724,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     // the INIT pass (r = c, s = A c) needs only c: on s1 while s2 factors E
     MNB_CUDA(cudaStreamWaitEvent(s1, eC, 0));
     launch_cg_init_pass(ctx, c_loc, xacc);
+    trace("INIT issued");
     SketchQr eq;
     cudaEvent_t eQ = ctx.timer_event();
     {
@@ -718,9 +738,11 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                         bad);
         MNB_CUDA(cudaEventRecord(eQ, ctx.stream));
     }
+    trace("QR(E)");
     MNB_CUDA(cudaStreamWaitEvent(s1, eQ, 0));
     LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false,
                           xacc, ax, /*init_done=*/true);
+    trace("CG");
     {
         float ms = 0.f;
         MNB_CUDA(cudaEventElapsedTime(&ms, eA, eS));
@@ -757,6 +779,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const double xnorm = std::sqrt(ls.xx);
     rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
     ctx.resolve_timers();
+    trace("resolve");
     rep.kernel_launches = ctx.launches - launches0;
     rep.total_seconds = now_s() - t_start;
 }

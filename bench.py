@@ -379,7 +379,8 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_all": step_ms, "higher_is_better": False,
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_step_median": statistics.median(step_ms),
+            "ms_per_step_all": step_ms, "higher_is_better": False,
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if cfg["real"] else "c128", "data": "synthetic (seeded, on device)",
             "config": config_json,

@@ -93,7 +93,8 @@ typedef struct {
     double residual_norm;    /* SolveReport::residual_norm = ||A x - b||                */
     int64_t lsq_iterations;  /* SolveReport::lsq_iterations                             */
     int32_t lsq_converged;   /* SolveReport::lsq_converged                              */
-    int32_t reserved0;
+    int32_t qr_path;         /* extension: sketch QR used, S in bits 0-3, E in bits 4-7:
+                                0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder     */
     int64_t sketch_size;     /* SolveReport::sketch_size                                */
     double lsq_tau;          /* SolveReport::lsq_tau                                    */
     /* ---- extensions (not in the reference report) ---- */

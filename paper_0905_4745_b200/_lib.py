@@ -42,7 +42,7 @@ class SolverConfigC(ctypes.Structure):
 class SolveReportC(ctypes.Structure):
     _fields_ = [("step_seconds", ctypes.c_double * 5), ("c_norm_ratio", ctypes.c_double),
                 ("residual_norm", ctypes.c_double), ("lsq_iterations", ctypes.c_int64),
-                ("lsq_converged", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("sketch_size", ctypes.c_int64),
+                ("lsq_converged", ctypes.c_int32), ("qr_path", ctypes.c_int32), ("sketch_size", ctypes.c_int64),
                 ("lsq_tau", ctypes.c_double), ("lsq_achieved_excess", ctypes.c_double),
                 ("param_seconds", ctypes.c_double), ("total_seconds", ctypes.c_double),
                 ("sketch_seconds", ctypes.c_double * 2), ("redistribute_seconds", ctypes.c_double),

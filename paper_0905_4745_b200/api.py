@@ -247,7 +247,7 @@ class SolveReport:
 
 
 def _report(rc: L.SolveReportC, x, c) -> SolveReport:
-    extra = {k: getattr(rc, k) for k in ("lsq_achieved_excess", "param_seconds", "total_seconds",
+    extra = {k: getattr(rc, k) for k in ("lsq_achieved_excess", "param_seconds", "total_seconds", "qr_path",
                                          "redistribute_seconds", "pcg_seconds", "pcg_pass_ms_sum",
                                          "pcg_pass_launches", "kernel_launches", "world_size")}
     extra["sketch_seconds"] = list(rc.sketch_seconds)

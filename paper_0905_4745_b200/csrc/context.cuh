@@ -112,6 +112,7 @@ struct Context {
     // workspaces
     DevBuf ws_x1, ws_x2, ws_slab, ws_pack;
     DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
+    bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
     DevBuf Rinv, Rinv_rows;
     DevBuf vec_m[8], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, state, resid, scratch;

@@ -124,4 +124,14 @@ void launch_chain_halos(const double2* cssn, int64_t n, int64_t chunk, int64_t n
     MNB_LAUNCH_CHECK();
 }
 
+__global__ void add_diagonal_kernel(double2* A, int64_t m, double shift) {
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < m) A[j + j * m].x += shift;
+}
+
+void launch_add_diagonal(double2* A, int64_t m, double shift, cudaStream_t stream) {
+    add_diagonal_kernel<<<ceil_div(m, 256), 256, 0, stream>>>(A, m, shift);
+    MNB_LAUNCH_CHECK();
+}
+
 }  // namespace mnb

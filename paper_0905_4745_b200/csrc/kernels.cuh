@@ -102,6 +102,8 @@ void launch_chain_halos(const double2* cssn, int64_t n, int64_t chunk, int64_t n
                         cudaStream_t stream);
 // zero the strictly lower triangle of an m x m column-major matrix
 void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream);
+// A_jj += shift (real), m x m column-major
+void launch_add_diagonal(double2* A, int64_t m, double shift, cudaStream_t stream);
 // out[0] = max_{i<=j} |A_ij - delta_ij| over the upper triangle (deterministic)
 void launch_max_offset_from_identity(const double2* A, int64_t m, double* out, cudaStream_t stream);
 void launch_copy_dups(double2* S, int64_t ldS, int64_t row0, int64_t rows, const int32_t* dups, int64_t ndups,

@@ -324,9 +324,12 @@ struct SketchQr {
     const double2* R;   // m x m upper triangle, leading dimension ldR
     int64_t ldR;
     bool householder;
+    int path = 0;       // 0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder
 };
 
-// CholeskyQR2 of the l x m sketch, R only (S is left intact):
+// CholeskyQR2 of the l x m sketch, R only (S is left intact) -- or, for sketches too ill-
+// conditioned for it, shifted CholeskyQR3 (a diagonal shift makes the first Cholesky safe up to
+// cond ~ 1/u; two more passes restore orthogonality).  CholeskyQR2:
 //   G = S^H S = R1^H R1,  Q1 = S R1^{-1},  Q1^H Q1 = R2^H R2,  R = R2 R1.
 // Two Gram passes on tensor-core ZHERK instead of Householder panels (~3x
 // fewer cycles at the BASELINE shapes).  R equals Householder's R up to a
@@ -336,13 +339,26 @@ struct SketchQr {
 // eps * cond(S)^2 < 1; returns false (caller falls back to Householder, as
 // the reference) when a Cholesky breaks down or Q1 = S R1^{-1} is not orthonormal
 // to 1e-3 (cond(S) above ~2e6).  On success ctx.qwork holds Q1 and ctx.R2 holds R2.
-bool cholqr2_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R) {
-    const auto* Sc = reinterpret_cast<const cuDoubleComplex*>(S);
+bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* Q = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
+    double2* Rp = dev<double2>(ctx.R2, size_t(m) * size_t(m));
     int* info = dev<int>(ctx.qr_info, 2);
     std::vector<double> diag(size_t(2 * m));
     int info_h = 0;
+    const double one = 1.0, zero = 0.0;
+    const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0);
+    auto herk = [&](const double2* X, double2* out) {
+        cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
+                                 reinterpret_cast<const cuDoubleComplex*>(X), int(l), &zero,
+                                 reinterpret_cast<cuDoubleComplex*>(out), int(m)),
+                     "zherk");
+    };
+    auto read_diag = [&](const double2* A) {
+        MNB_CUDA(cudaMemcpy2DAsync(diag.data(), 16, A, size_t(m + 1) * 16, 16, size_t(m), cudaMemcpyDeviceToHost,
+                                   ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    };
     auto potrf = [&](double2* A) {
         size_t dws = 0, hws = 0;
         cusolver_check(cusolverDnXpotrf_bufferSize(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m,
@@ -356,54 +372,64 @@ bool cholqr2_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R)
         launch_zero_lower(A, m, ctx.stream);
         ctx.launches += 1;
         MNB_CUDA(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-        MNB_CUDA(cudaMemcpy2DAsync(diag.data(), 16, A, size_t(m + 1) * 16, 16, size_t(m), cudaMemcpyDeviceToHost,
-                                   ctx.stream));
-        MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+        read_diag(A);
     };
-    const double one = 1.0, zero = 0.0;
-    const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0);
-    // pass 1
-    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one, Sc, int(l), &zero,
-                             reinterpret_cast<cuDoubleComplex*>(G), int(m)),
-                 "zherk");
+    auto trsm_q = [&](const double2* Rt) {  // Q <- Q Rt^{-1}
+        cublas_check(cublasZtrsm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_NON_UNIT, int(l), int(m), &cone,
+                                 reinterpret_cast<const cuDoubleComplex*>(Rt), int(m),
+                                 reinterpret_cast<cuDoubleComplex*>(Q), int(l)),
+                     "ztrsm");
+    };
+    // pass 1: G = S^H S (+ shift) = R1^H R1, Q1 = S R1^{-1}
+    herk(S, G);
+    if (shifted) {
+        // shifted CholeskyQR (Fukaya et al.): s = 11 (l m + m (m + 1)) u ||S||^2, ||S||_2^2 <= trace(G)
+        read_diag(G);
+        double tr = 0.0;
+        for (int64_t j = 0; j < m; ++j) tr += diag[size_t(2 * j)];
+        const double shift = 11.0 * (double(l) * double(m) + double(m) * double(m + 1)) * kEps * tr;
+        launch_add_diagonal(G, m, shift, ctx.stream);
+        ctx.launches += 1;
+    }
     potrf(G);
     if (info_h != 0) return false;
-    double dmax = 0.0, dmin = 1e300;
-    for (int64_t j = 0; j < m; ++j) {
-        const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
-        dmax = std::max(dmax, a);
-        dmin = std::min(dmin, a);
+    if (!shifted) {
+        double dmax = 0.0, dmin = 1e300;
+        for (int64_t j = 0; j < m; ++j) {
+            const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
+            dmax = std::max(dmax, a);
+            dmin = std::min(dmin, a);
+        }
+        if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
     }
-    if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
     MNB_CUDA(cudaMemcpyAsync(Q, S, size_t(l) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
-    cublas_check(cublasZtrsm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                             int(l), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(G), int(m),
-                             reinterpret_cast<cuDoubleComplex*>(Q), int(l)),
-                 "ztrsm");
-    // pass 2: R2 = chol(Q1^H Q1).  Q1 must be nearly orthonormal (|G2 - I| ~ eps cond(S)^2) for
-    // the product R2 R1 to be accurate; otherwise the sketch is too ill-conditioned for CholeskyQR2.
-    double2* R2 = dev<double2>(ctx.R2, size_t(m) * size_t(m));
-    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
-                             reinterpret_cast<const cuDoubleComplex*>(Q), int(l), &zero,
-                             reinterpret_cast<cuDoubleComplex*>(R2), int(m)),
-                 "zherk");
-    double* dev_max = dev<double>(ctx.scratch, 512);
-    launch_max_offset_from_identity(R2, m, dev_max, ctx.stream);
-    ctx.launches += 1;
-    double gmax = 0.0;
-    MNB_CUDA(cudaMemcpyAsync(&gmax, dev_max, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-    MNB_CUDA(cudaStreamSynchronize(ctx.stream));
-    if (!(gmax < 1e-3)) return false;
-    potrf(R2);
-    if (info_h != 0) return false;
-    // R = R2 R1 (R1 in G; both upper with zeroed lower parts)
+    trsm_q(G);
     MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
-    cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                             int(m), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(R2), int(m),
-                             reinterpret_cast<const cuDoubleComplex*>(R), int(m), reinterpret_cast<cuDoubleComplex*>(R),
-                             int(m)),
-                 "ztrmm");
-    return true;
+    // passes 2 (and 3): R_p = chol(Q^H Q); R <- R_p R; on the last pass Q must already be
+    // orthonormal to 1e-3 (|Q^H Q - I| ~ eps cond^2) for R to be accurate -- else Householder.
+    const int passes = shifted ? 3 : 2;
+    for (int p = 2; p <= passes; ++p) {
+        herk(Q, Rp);
+        if (p == passes) {
+            double* dev_max = dev<double>(ctx.scratch, 512);
+            launch_max_offset_from_identity(Rp, m, dev_max, ctx.stream);
+            ctx.launches += 1;
+            double gmax = 0.0;
+            MNB_CUDA(cudaMemcpyAsync(&gmax, dev_max, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+            MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+            if (!(gmax < 1e-3)) return false;
+        }
+        potrf(Rp);
+        if (info_h != 0) return false;
+        if (p < passes) trsm_q(Rp);
+        cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                 CUBLAS_DIAG_NON_UNIT, int(m), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(Rp),
+                                 int(m), reinterpret_cast<const cuDoubleComplex*>(R), int(m),
+                                 reinterpret_cast<cuDoubleComplex*>(R), int(m)),
+                     "ztrmm");
+    }
+    return true;  // ctx.qwork holds Q_{passes-1}, ctx.R2 the last R_p:  Q = Q_{passes-1} R_p^{-1}
 }
 
 // QR of a finished l x m sketch on ctx.stream (CholeskyQR2, else Householder); qr_s += device time.
@@ -414,11 +440,26 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
     cudaEvent_t e1 = ctx.timer_event(), e2 = ctx.timer_event();
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
     SketchQr out{S, tau, R, m, false};
-    if (!(ctx.cholqr && cholqr2_r(ctx, S, l, m, R))) {
+    out.path = 0;
+    // CholeskyQR2; if the sketch is too ill-conditioned, shifted CholeskyQR3 (and once a sketch of
+    // this solve needed it, the next one starts there); Householder (the reference's) as the last resort
+    bool done = false;
+    if (ctx.cholqr) {
+        if (!ctx.qr_shifted) {
+            done = cholqr_r(ctx, S, l, m, R, false);
+            if (!done) ctx.qr_shifted = true;
+        }
+        if (!done) {
+            done = cholqr_r(ctx, S, l, m, R, true);
+            out.path = 1;
+        }
+    }
+    if (!done) {
         qr_in_place(ctx, S, l, m, tau);
         out.R = S;
         out.ldR = l;
         out.householder = true;
+        out.path = 2;
     }
     MNB_CUDA(cudaEventRecord(e2, ctx.stream));
     MNB_CUDA(cudaEventSynchronize(e2));
@@ -510,6 +551,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const double t_start = now_s();
     ctx.timers.clear();  // drop timers of an aborted call (they point into its report)
     ctx.timer_next = 0;
+    ctx.qr_shifted = false;
     validate_matrix_set(ctx);
     const int64_t m = ctx.m, n = ctx.n_global;
     // ProblemInstance::validate (src/solver.cpp:37-48); A's finiteness is checked on the device below.
@@ -752,6 +794,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     }
     rep.qr_seconds[0] = qr_s0;
     rep.qr_seconds[1] = qr_s1;
+    rep.qr_path = sq.path | (eq.path << 4);
     rep.lsq_iterations = ls.iterations;
     rep.lsq_converged = ls.converged ? 1 : 0;
     rep.lsq_achieved_excess = ls.achieved_excess;
@@ -790,6 +833,7 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
     validate_matrix_set(ctx);
     ctx.timers.clear();
     ctx.timer_next = 0;
+    ctx.qr_shifted = false;
     const int64_t m = ctx.m, n = ctx.n_global;  // B = A^H is n x m
     // src/lsq.cpp:45-53
     if (m < 1 || n <= m) throw Error(MNB_ERR_INVALID_ARGUMENT, "solve_least_squares: B must be tall (n > m >= 1)");

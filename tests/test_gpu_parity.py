@@ -143,9 +143,10 @@ def test_solve_real_matrix(ctx):
 @pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (128, 8192, 1e8, 1e-10)])
 def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
     """The sketch QRs run CholeskyQR2 (tensor-core ZHERK) when the sketch is
-    well enough conditioned and fall back to Householder (the reference's
-    HouseholderQR, src/solver.cpp:86, src/lsq.cpp:58) otherwise; both must give
-    the same solve."""
+    well enough conditioned, shifted CholeskyQR3 when it is not, and
+    Householder (the reference's HouseholderQR, src/solver.cpp:86,
+    src/lsq.cpp:58) as the last resort / with MNB_QR=householder; all must
+    give the same solve."""
     A, b = make_instance(m, n, kappa, seed=m + 3)
     cfg = mn.SolverConfig(epsilon=eps, seed=42)
     reps = {}
@@ -155,6 +156,9 @@ def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
         reps[mode] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
         c.close()
     a, h = reps["cholqr2"], reps["householder"]
+    # path taken: CholeskyQR2 (0) for well-conditioned sketches, shifted CholeskyQR3 (1) at 1e8
+    assert (a.extra["qr_path"] & 15) == (1 if kappa >= 1e8 else 0)
+    assert h.extra["qr_path"] == 2 | (2 << 4)
     p = O.solve_classical(A, b)
     assert rel(a.x, p) <= solve_tol(eps, kappa)
     assert rel(a.x, h.x) <= solve_tol(eps, kappa)

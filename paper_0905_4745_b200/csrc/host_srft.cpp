@@ -8,7 +8,12 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <deque>
 #include <exception>
+#include <future>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 
@@ -31,6 +36,131 @@ enum : uint64_t { kD = 1, kSample = 2, kTheta = 3, kThetaTilde = 4, kPerm = 5, k
 // Scan halo: stop once the carried product of |sin| drops below 2^-70.
 constexpr double kHaloThreshold = 0x1.0p-70;
 }  // namespace
+
+// Persistent host worker pool.  Spawning a fresh set of threads per operator
+// (two per solve) costs thread creation plus 8 MiB stack mmap/munmap each,
+// whose TLB shootdowns stalled the thread driving the GPU by milliseconds.
+// run(width, fn): up to width-1 pool workers join the calling thread in
+// calling fn (fn pulls its own work items and returns when none are left).
+class WorkerPool {
+public:
+    static WorkerPool& get() {
+        static WorkerPool pool(int(std::max(1u, std::min(64u, std::thread::hardware_concurrency()))));
+        return pool;
+    }
+    void run(int width, const std::function<void()>& fn) {
+        auto job = std::make_shared<Job>();
+        job->fn = &fn;
+        job->slots = std::max(0, std::min(width - 1, int(workers_.size())));
+        if (job->slots > 0) {
+            std::lock_guard<std::mutex> g(mu_);
+            jobs_.push_back(job);
+            cv_.notify_all();
+        }
+        fn();
+        {
+            std::unique_lock<std::mutex> g(mu_);
+            job->slots = 0;  // closed: no new helpers
+            jobs_.erase(std::remove(jobs_.begin(), jobs_.end(), job), jobs_.end());
+            done_.wait(g, [&] { return job->active == 0; });
+        }
+    }
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+            cv_.notify_all();
+        }
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    struct Job {
+        const std::function<void()>* fn = nullptr;
+        int slots = 0, active = 0;
+    };
+    explicit WorkerPool(int n) {
+        for (int i = 0; i < n - 1; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        std::unique_lock<std::mutex> g(mu_);
+        for (;;) {
+            cv_.wait(g, [&] {
+                if (stop_) return true;
+                for (auto& j : jobs_)
+                    if (j->slots > 0) return true;
+                return false;
+            });
+            if (stop_) return;
+            std::shared_ptr<Job> job;
+            for (auto& j : jobs_)
+                if (j->slots > 0) {
+                    job = j;
+                    break;
+                }
+            --job->slots;
+            ++job->active;
+            g.unlock();
+            (*job->fn)();
+            g.lock();
+            if (--job->active == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::shared_ptr<Job>> jobs_;
+    bool stop_ = false;
+};
+
+// One persistent thread for host_async (tasks run in submission order).
+class BackgroundThread {
+public:
+    static BackgroundThread& get() {
+        static BackgroundThread t;
+        return t;
+    }
+    std::future<void> submit(std::function<void()> fn) {
+        std::packaged_task<void()> task(std::move(fn));
+        auto fut = task.get_future();
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            q_.push_back(std::move(task));
+        }
+        cv_.notify_one();
+        return fut;
+    }
+    ~BackgroundThread() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_one();
+        th_.join();
+    }
+
+private:
+    BackgroundThread() : th_([this] { loop(); }) {}
+    void loop() {
+        std::unique_lock<std::mutex> g(mu_);
+        for (;;) {
+            cv_.wait(g, [&] { return stop_ || !q_.empty(); });
+            if (q_.empty()) return;
+            auto task = std::move(q_.front());
+            q_.pop_front();
+            g.unlock();
+            task();
+            g.lock();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::packaged_task<void()>> q_;
+    bool stop_ = false;
+    std::thread th_;
+};
+
+std::future<void> host_async(std::function<void()> fn) { return BackgroundThread::get().submit(std::move(fn)); }
 
 RandomStream::RandomStream(uint64_t seed) : seed_(seed) {
     uint64_t sm = seed;
@@ -145,28 +275,29 @@ void SrftHost::layout() {
 // that the neglected contribution is below kHaloThreshold (the carry of the
 // chain recurrence decays by |sin(theta_j)| per step).
 static void chain_halos(const double* cssn, int64_t n, const ChainChunks& ch, int32_t* fwd, int32_t* adj) {
-    const int threads = int(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-    std::vector<std::thread> pool;
-    for (int t = 0; t < threads; ++t)
-        pool.emplace_back([&, t] {
-    for (int64_t c = t; c < ch.nchunks; c += threads) {
-        const int64_t i0 = c * ch.chunk, i1 = std::min(n, i0 + ch.chunk);
-        // forward chain: carry flows from high to low indices
-        int64_t t = i1;
-        if (i1 >= n) t = n - 1;
-        else {
-            double p = 1.0;
-            while (t < n - 1 && p > kHaloThreshold) { p *= std::fabs(cssn[2 * t + 1]); ++t; }
+    std::atomic<int64_t> next{0};
+    const std::function<void()> work = [&] {
+        for (int64_t c; (c = next.fetch_add(64)) < ch.nchunks;) {
+            const int64_t ce = std::min(ch.nchunks, c + 64);
+            for (; c < ce; ++c) {
+                const int64_t i0 = c * ch.chunk, i1 = std::min(n, i0 + ch.chunk);
+                // forward chain: carry flows from high to low indices
+                int64_t t = i1;
+                if (i1 >= n) t = n - 1;
+                else {
+                    double p = 1.0;
+                    while (t < n - 1 && p > kHaloThreshold) { p *= std::fabs(cssn[2 * t + 1]); ++t; }
+                }
+                fwd[c] = int32_t(t);
+                // adjoint chain: carry flows from low to high indices
+                int64_t s = i0;
+                double p = 1.0;
+                while (s > 0 && p > kHaloThreshold) { --s; p *= std::fabs(cssn[2 * s + 1]); }
+                adj[c] = int32_t(s);
+            }
         }
-        fwd[c] = int32_t(t);
-        // adjoint chain: carry flows from low to high indices
-        int64_t s = i0;
-        double p = 1.0;
-        while (s > 0 && p > kHaloThreshold) { --s; p *= std::fabs(cssn[2 * s + 1]); }
-        adj[c] = int32_t(s);
-    }
-        });
-    for (auto& th : pool) th.join();
+    };
+    WorkerPool::get().run(int(std::min<int64_t>(16, 1 + ch.nchunks / 256)), work);
 }
 
 void SrftHost::derive() {
@@ -204,23 +335,6 @@ void SrftHost::derive() {
     }
 }
 
-namespace {
-// Run fn(i) for i in [0, count) on up to `threads` workers.
-template <class F>
-void parallel_for(int64_t count, int threads, F&& fn) {
-    if (count <= 0) return;
-    threads = int(std::min<int64_t>(threads, count));
-    if (threads <= 1) { for (int64_t i = 0; i < count; ++i) fn(i); return; }
-    std::atomic<int64_t> next{0};
-    std::vector<std::thread> pool;
-    pool.reserve(size_t(threads));
-    for (int t = 0; t < threads; ++t)
-        pool.emplace_back([&] {
-            for (int64_t i; (i = next.fetch_add(1)) < count;) fn(i);
-        });
-    for (auto& th : pool) th.join();
-}
-}  // namespace
 
 void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, int sampling,
                      const BlobAlloc& alloc, const BlobFree& release, int threads) {
@@ -315,12 +429,10 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         }
     };
     {
-        // one worker per 2K indices up to the pool size (thread start-up outweighs tiny operators)
+        // one worker per 2K indices up to `threads` (tiny operators are drawn in microseconds)
         const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, n / 2048)));
-        std::vector<std::thread> pool;
-        for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
-        worker();
-        for (auto& th : pool) th.join();
+        const std::function<void()> work = worker;
+        WorkerPool::get().run(nt, work);
     }
     if (error) std::rethrow_exception(error);
     op.derive();

@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <future>
 #include <vector>
 
 namespace mnb {
@@ -86,6 +87,9 @@ using BlobFree = std::function<void(unsigned char*)>;
 // with the eight tagged substreams (srft.cpp:13-22) drawn concurrently and
 // the cos/sin of finalize (srft.cpp:80-93) evaluated in parallel chunks.
 // Throws mnb::Error(MNB_ERR_INVALID_ARGUMENT) like the reference.
+// Run fn on a persistent background host thread (no per-solve thread creation).
+std::future<void> host_async(std::function<void()> fn);
+
 void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, int sampling,
                      const BlobAlloc& alloc, const BlobFree& release, int threads = 0);
 

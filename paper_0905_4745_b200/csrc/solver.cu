@@ -630,6 +630,11 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         t_param_Tp = now_s() - s;
     };
     std::future<void> fut_Tp;
+    // host_async futures do not block on destruction: join the draw before T/T' go out of scope
+    struct JoinGuard {
+        std::future<void>& f;
+        ~JoinGuard() { if (f.valid()) f.wait(); }
+    } join_Tp{fut_Tp};
     SrftDev& Td = ctx.op_dev[0];
     SrftDev& Tpd = ctx.op_dev[1];
     if (pipelined) {
@@ -647,7 +652,8 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         };
         issue(0);
         const double tp0 = now_s();
-        auto f1 = std::async(std::launch::async, build_T, std::max(1, hw / 2));
+        auto f1 = host_async([&] { build_T(std::max(1, hw / 2)); });
+        JoinGuard join_T{f1};
         build_Tp(std::max(1, hw - hw / 2));
         f1.get();
         (void)tp0;
@@ -656,7 +662,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         for (size_t k = 1; k < slabs.size(); ++k) issue(k);
     } else {
         build_T(hw);
-        fut_Tp = std::async(std::launch::async, build_Tp, std::max(1, hw / 2));
+        fut_Tp = host_async([&] { build_Tp(std::max(1, hw / 2)); });
     }
 
     // Streams: the sketches and the CG passes (memory-bound) run on ctx.stream; with one GPU the

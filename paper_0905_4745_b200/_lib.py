@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libminnorm_b200.so")
+# MNB_LIB_PATH: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("MNB_LIB_PATH") or os.path.join(_HERE, "libminnorm_b200.so")
 
 MNB_OK = 0
 MNB_ERR_INVALID_ARGUMENT = 1

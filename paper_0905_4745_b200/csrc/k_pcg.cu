@@ -160,10 +160,13 @@ __host__ __device__ constexpr int log2c() { return V <= 1 ? 0 : 1 + log2c<V / 2>
 // BASELINE shape), so shared-memory offsets are immediates and no row is
 // masked; GT == 0 is the generic kernel (runtime G, masked rows).
 template <typename AT, int EPL, int GT>
-__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int g_rt, int stages, int64_t C,
+__global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs p, int g_rt, int stages, int64_t C_rt,
                                                                int64_t per) {
     constexpr int K = batch_cols<AT, EPL>();
     constexpr int V = 2 * K;
+    // exact shapes: one batch per group per stage (plan_pcg_pass), so the stage
+    // geometry folds to immediates
+    const int64_t C = GT ? int64_t(kConsumerWarps / (GT ? GT : 1)) * K : C_rt;
     extern __shared__ __align__(128) unsigned char smem[];
     if (p.state && p.state->done) return;  // uniform: converged loops cost one launch
     const int G = GT ? GT : g_rt;
@@ -220,7 +223,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
     const int gq = warp / G, wig = warp % G;
     const int row0 = wig * 32 + lane, rstep = 32 * G;
     double2 wreg[EPL], sacc[EPL];
-#define ROW(e) (row0 + (e) * rstep)
+    // Real A at exact shapes: a lane owns EPL/2 PAIRS of adjacent rows, so the
+    // stage is read with 16-byte shared loads (half the load instructions).
+    constexpr bool PAIR = sizeof(AT) == 8 && GT != 0 && EPL % 2 == 0;
+#define ROW(e) (PAIR ? 2 * (row0 + ((e) >> 1) * rstep) + ((e) & 1) : row0 + (e) * rstep)
 #define ROW_OK(e) (GT != 0 || ROW(e) < mi)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
@@ -243,15 +249,34 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
 
         // The slot of batch s is released when batch s+1 is loaded, so the
         // epilogue of batch s can still read its t_old / r / c from the stage.
-        auto load = [&](int64_t cc, bool release_prev) {
-            if (release_prev) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[cslot]);
-            }
-            mbar_wait(&full[lslot], lph);
-            const unsigned char* st = smem + lslot * L.stage_bytes;
-            const AT* tA = reinterpret_cast<const AT*>(st + L.tileA) + gq * K * mi + row0;
-            if (cc == C) {  // uniform: every stage but possibly the last
+        // a[][] <- the batch's columns from stage st (cc columns in the stage)
+        auto fetch = [&](const unsigned char* st, int64_t cc) {
+            const AT* tA = reinterpret_cast<const AT*>(st + L.tileA) + gq * K * mi + (PAIR ? 2 * row0 : row0);
+            if constexpr (PAIR) {
+                const int have = cc == C ? K : int(cc) - gq * K;
+                if (cc == C) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+#pragma unroll
+                        for (int e = 0; e < EPL; e += 2) {
+                            const double2 pr = *reinterpret_cast<const double2*>(
+                                reinterpret_cast<const double*>(tA) + k * mi + e * rstep);
+                            reinterpret_cast<double*>(&a[k][e])[0] = pr.x;
+                            reinterpret_cast<double*>(&a[k][e + 1])[0] = pr.y;
+                        }
+                    return;
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int e = 0; e < EPL; e += 2) {
+                        const double2 pr = k < have ? *reinterpret_cast<const double2*>(
+                                                          reinterpret_cast<const double*>(tA) + k * mi + e * rstep)
+                                                    : make_double2(0.0, 0.0);
+                        reinterpret_cast<double*>(&a[k][e])[0] = pr.x;
+                        reinterpret_cast<double*>(&a[k][e + 1])[0] = pr.y;
+                    }
+            } else if (cc == C) {  // uniform: every stage but possibly the last
 #pragma unroll
                 for (int k = 0; k < K; ++k)
 #pragma unroll
@@ -264,6 +289,16 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
                     for (int e = 0; e < EPL; ++e)
                         a[k][e] = (k < have && ROW_OK(e)) ? tA[k * mi + e * rstep] : zero_of<AT>();
             }
+        };
+        // The slot of batch s is released when batch s+1 is loaded, so the
+        // epilogue of batch s can still read its t_old / r / c from the stage.
+        auto load = [&](int64_t cc, bool release_prev) {
+            if (release_prev) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[cslot]);
+            }
+            mbar_wait(&full[lslot], lph);
+            fetch(smem + lslot * L.stage_bytes, cc);
             cslot = lslot;
             if (++lslot == stages) {
                 lslot = 0;
@@ -327,6 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1) pcg_pass_kernel(const PcgPassArgs
             } else {
                 gather_t(buf, t);
             }
+#ifdef MNB_PCG_REREAD
+            // the batch is still in its stage: read it again rather than hold it across the barrier
+            if (!init) fetch(cst, cc);
+#endif
 #pragma unroll
             for (int k = 0; k < K; ++k)
 #pragma unroll

@@ -81,6 +81,14 @@ struct SrftDev {
     int64_t vec_chunk = 0, vec_nchunks = 0;
     DevBuf fb_csr;        // kept frequencies per f2 for the pruned FFT pass B: [n2+1 offsets][(f1, slot) pairs]
     int64_t fb_n2 = 0;
+    // page-locked staging of the small host-built tables (dups, fb_csr): async uploads, no
+    // pageable copies (which serialise the host behind the stream)
+    PinnedBuf stage;
+    cudaEvent_t stage_free = nullptr;  // the last upload out of `stage` has completed
+    SrftDev() = default;
+    SrftDev(const SrftDev&) = delete;
+    SrftDev& operator=(const SrftDev&) = delete;
+    ~SrftDev() { if (stage_free) cudaEventDestroy(stage_free); }
     template <class T> const T* at(size_t off) const { return reinterpret_cast<const T*>(blob.as<unsigned char>() + off); }
 };
 
@@ -119,6 +127,9 @@ struct Context {
     DevBuf rhs, flag, out_c;
     int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
     PinnedBuf pin_params[2], pin_small;
+    struct SlabCache {
+        int64_t n = -1, rows = -1, l = -1, m = -1, Ms = 0;
+    } slab_cache;  // sketch slab height per shape (srft_gpu.cu sketch_block)
     SrftDev op_dev[3];  // device copies of the operators: [0] T, [1] T', [2] standalone SRFT calls (grow-only)
     std::vector<cudaEvent_t> events;
     // deferred kernel timers (EventTimer): event pool + pending (start, stop, accumulator)

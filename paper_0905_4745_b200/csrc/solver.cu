@@ -208,16 +208,17 @@ void launch_cg_init_pass(Context& ctx, const double2* c, double2* x) {
 }
 
 LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
-                 double dup, double2* y, bool want_norms, double2* x, double2* ax, bool init_done) {
+                 double dup, double2* y, bool want_norms, double2* x, double2* ax, bool init_done,
+                 bool rinv_ready) {
     const int64_t m = ctx.m, n = ctx.n_local;
     LsqResult res;
     const double t0 = now_s();
     // explicit R'^{-1} (consistent forward/adjoint preconditioner)
     double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
     double2* Rinv_rows = dev<double2>(ctx.Rinv_rows, size_t(m) * size_t(m));
-    MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, Rtop, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
-                               cudaMemcpyDeviceToDevice, ctx.stream));
-    {
+    if (!rinv_ready) {  // (the one-pass Cholesky preconditioner already left R'^{-1} in ctx.Rinv)
+        MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, Rtop, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
+                                   cudaMemcpyDeviceToDevice, ctx.stream));
         size_t dws = 0, hws = 0;
         cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
                                                    CUDA_C_64F, Rinv, m, &dws, &hws),
@@ -324,7 +325,8 @@ struct SketchQr {
     const double2* R;   // m x m upper triangle, leading dimension ldR
     int64_t ldR;
     bool householder;
-    int path = 0;       // 0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder
+    int path = 0;       // 0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder, 3 one Cholesky pass (preconditioner)
+    bool rinv_ready = false;  // path 3: R^{-1} already in ctx.Rinv
 };
 
 // CholeskyQR2 of the l x m sketch, R only (S is left intact) -- or, for sketches too ill-
@@ -339,7 +341,7 @@ struct SketchQr {
 // eps * cond(S)^2 < 1; returns false (caller falls back to Householder, as
 // the reference) when a Cholesky breaks down or Q1 = S R1^{-1} is not orthonormal
 // to 1e-3 (cond(S) above ~2e6).  On success ctx.qwork holds Q1 and ctx.R2 holds R2.
-bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted) {
+bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted, bool* precond_only) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* Q = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
     double2* Rp = dev<double2>(ctx.R2, size_t(m) * size_t(m));
@@ -403,6 +405,33 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         }
         if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
     }
+    if (precond_only && *precond_only) {
+        // The CG preconditioner needs only an R1 with E R1^{-1} near-orthonormal -- and
+        // |Q1^H Q1 - I| ~ u cond(E)^2 <= u ||R1||_F^2 ||R1^{-1}||_F^2.  When that bound is below
+        // 1e-3 one Cholesky pass is enough (the CG rate and its stopping bound sigma_min(B R'^{-1})
+        // >= 1, lsq.cpp:66-69, move by < 1e-3): no Q1, no second pass, and R'^{-1} (which the CG
+        // forms anyway) is left in ctx.Rinv.
+        double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
+        MNB_CUDA(cudaMemcpyAsync(Rinv, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
+                                                   CUDA_C_64F, Rinv, m, &dws, &hws),
+                       "trtri_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXtrtri(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m, CUDA_C_64F, Rinv,
+                                        m, work, dws, ctx.host_work.data(), hws, info),
+                       "trtri");
+        double nr = 0.0, nri = 0.0;  // lower triangles are zero
+        cublas_check(cublasDznrm2(ctx.cublas, int(m * m), reinterpret_cast<const cuDoubleComplex*>(G), 1, &nr), "dznrm2");
+        cublas_check(cublasDznrm2(ctx.cublas, int(m * m), reinterpret_cast<const cuDoubleComplex*>(Rinv), 1, &nri),
+                     "dznrm2");
+        if (kEps * nr * nr * nri * nri <= 1e-3) {
+            MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+            return true;
+        }
+        *precond_only = false;  // R'^{-1} in ctx.Rinv is stale: the full factorization follows
+    }
     MNB_CUDA(cudaMemcpyAsync(Q, S, size_t(l) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     trsm_q(G);
     MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -433,7 +462,8 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
 }
 
 // QR of a finished l x m sketch on ctx.stream (CholeskyQR2, else Householder); qr_s += device time.
-SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBuf& Rbuf, double* qr_s) {
+SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBuf& Rbuf, double* qr_s,
+                      bool precond = false) {
     const int64_t m = ctx.m;
     double2* tau = dev<double2>(taubuf, size_t(m));
     double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
@@ -446,11 +476,16 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
     bool done = false;
     if (ctx.cholqr) {
         if (!ctx.qr_shifted) {
-            done = cholqr_r(ctx, S, l, m, R, false);
+            bool one_pass = precond;
+            done = cholqr_r(ctx, S, l, m, R, false, &one_pass);
+            if (done && one_pass) {
+                out.path = 3;
+                out.rinv_ready = true;
+            }
             if (!done) ctx.qr_shifted = true;
         }
         if (!done) {
-            done = cholqr_r(ctx, S, l, m, R, true);
+            done = cholqr_r(ctx, S, l, m, R, true, nullptr);
             out.path = 1;
         }
     }
@@ -470,14 +505,14 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
 }
 
 SketchQr sketch_and_qr(Context& ctx, const SrftDev& op, DevBuf& Sbuf, DevBuf& taubuf, DevBuf& Rbuf, double* kernel_ms,
-                       double* sketch_s, double* qr_s, double* redistribute_s) {
+                       double* sketch_s, double* qr_s, double* redistribute_s, bool precond = false) {
     const int64_t l = op.host->l, m = ctx.m;
     double2* S = dev<double2>(Sbuf, size_t(l) * size_t(m));
     cudaEvent_t e0 = ctx.timer_event(), e1 = ctx.timer_event();
     MNB_CUDA(cudaEventRecord(e0, ctx.stream));
     sketch_matrix(ctx, op, S, kernel_ms, redistribute_s);
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
-    SketchQr out = qr_of_sketch(ctx, S, l, taubuf, Rbuf, qr_s);
+    SketchQr out = qr_of_sketch(ctx, S, l, taubuf, Rbuf, qr_s, precond);
     float a = 0.f;
     MNB_CUDA(cudaEventElapsedTime(&a, e0, e1));
     if (sketch_s) *sketch_s += a * 1e-3;
@@ -603,7 +638,12 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const int sampling = cfg.sampling;
     const RandomStream root(cfg.seed);
     const uint64_t seed_T = root.derive_seed(11), seed_Tp = root.derive_seed(12);  // src/solver.cpp:19
-    const int hw = int(std::max(2u, std::thread::hardware_concurrency()));
+    // host threads for the parameter draws (MNB_HOST_THREADS overrides the core count)
+    static const int hw = [] {
+        const char* e = std::getenv("MNB_HOST_THREADS");
+        const int v = e ? std::atoi(e) : 0;
+        return v >= 2 ? v : int(std::max(2u, std::thread::hardware_concurrency()));
+    }();
     // Deferred host A (MNB_HOST_ASYNC, one GPU): copy it in row slabs on a side stream now; both
     // sketches then run slab by slab as the rows land, so the H2D hides the parameter draws, the
     // sketches and most of Step 1.  Otherwise A is already resident.
@@ -778,7 +818,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     {
         OnStream on(ctx, s2);
         MNB_CUDA(cudaStreamWaitEvent(s2, eE, 0));
-        eq = qr_of_sketch(ctx, Ebuf, l, ctx.tau_E, ctx.R_E, &qr_s1);
+        eq = qr_of_sketch(ctx, Ebuf, l, ctx.tau_E, ctx.R_E, &qr_s1, /*precond=*/true);
         if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
             throw Error(MNB_ERR_RANK_DEFICIENCY,
                         "solve_least_squares: sketch QR found " + std::to_string(bad) +
@@ -789,7 +829,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     trace("QR(E)");
     MNB_CUDA(cudaStreamWaitEvent(s1, eQ, 0));
     LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false,
-                          xacc, ax, /*init_done=*/true);
+                          xacc, ax, /*init_done=*/true, eq.rinv_ready);
     trace("CG");
     {
         float ms = 0.f;
@@ -853,14 +893,14 @@ void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_confi
                     [&](size_t bytes) { return pinned_alloc(ctx.pin_params[1], bytes); }, [](unsigned char*) {}, 0);
     SrftDev& Tpd = ctx.op_dev[1];
     upload_srft(ctx, Tp, Tpd);
-    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, nullptr, nullptr, nullptr, nullptr);
+    SketchQr eq = sketch_and_qr(ctx, Tpd, ctx.sk_E, ctx.tau_E, ctx.R_E, nullptr, nullptr, nullptr, nullptr, true);
     if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
         throw Error(MNB_ERR_RANK_DEFICIENCY,
                     "solve_least_squares: sketch QR found " + std::to_string(bad) + " numerically dependent columns",
                     bad);
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
     LsqResult ls = run_cg(ctx, c_dev, eq.R, eq.ldR, cfg.tau, cfg.max_iterations, double(Tp.max_mult), y,
-                          residual_norms != nullptr, nullptr, nullptr, false);
+                          residual_norms != nullptr, nullptr, nullptr, false, eq.rinv_ready);
     MNB_CUDA(cudaMemcpyAsync(y_host, y, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
     sync(ctx);
     sol.achieved_excess = ls.achieved_excess;

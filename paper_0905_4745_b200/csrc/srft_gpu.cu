@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <cstring>
 #include "context.cuh"
 
 namespace mnb {
@@ -268,13 +269,19 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
     dev.host = &op;
     dev.blob.ensure(op.device_bytes);
     MNB_CUDA(cudaMemcpyAsync(dev.blob.p, op.blob, op.device_bytes, cudaMemcpyHostToDevice, ctx.stream));
-    dev.ndups = int64_t(op.dups.size() / 2);
+    const FftPlan& P = ctx.fft_plan(op.n);
+    const int64_t n2 = P.single ? 0 : P.n2;
+    // staging: [dups][csr offsets (n2 + 1)][(f1, slot) pairs (<= 2 l)]
+    const size_t n_dups = op.dups.size(), n_csr = n2 ? size_t(n2 + 1) + 2 * size_t(op.l) : 0;
+    if (dev.stage_free) MNB_CUDA(cudaEventSynchronize(dev.stage_free));  // previous upload out of the stage
+    else MNB_CUDA(cudaEventCreateWithFlags(&dev.stage_free, cudaEventDisableTiming));
+    int32_t* stage = static_cast<int32_t*>(dev.stage.ensure(std::max<size_t>(16, (n_dups + n_csr) * 4)));
+    dev.ndups = int64_t(n_dups / 2);
     if (dev.ndups) {
-        dev.dups.ensure(op.dups.size() * 4);
-        MNB_CUDA(cudaMemcpyAsync(dev.dups.p, op.dups.data(), op.dups.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
-        MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // op.dups is pageable
+        std::memcpy(stage, op.dups.data(), n_dups * 4);
+        dev.dups.ensure(n_dups * 4);
+        MNB_CUDA(cudaMemcpyAsync(dev.dups.p, stage, n_dups * 4, cudaMemcpyHostToDevice, ctx.stream));
     }
-    ctx.fft_plan(op.n);
     // per-step records of the two sketch H stages (k_hchain.cu)
     const int64_t n = op.n;
     double2* rec1 = static_cast<double2*>(dev.chain_rec[0].ensure(size_t(n) * 48));
@@ -295,19 +302,18 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
     }
     // kept frequencies grouped by f2 = F mod n2 for the pruned pass B (first occurrence of each F;
     // repeated samples are copied afterwards, launch_copy_dups)
-    const FftPlan& P = ctx.fft_plan(n);
     dev.fb_n2 = 0;
-    if (!P.single) {
-        const int64_t n2 = P.n2;
+    if (n2) {
         const int64_t* s64 = op.at<int64_t>(op.off_sample64);
         const int32_t* sel = op.at<int32_t>(op.off_sel);
-        std::vector<int32_t> csr(size_t(n2 + 1) + 2 * size_t(op.l), 0);
-        int32_t* off = csr.data();
+        int32_t* csr = stage + n_dups;
+        std::memset(csr, 0, n_csr * 4);
+        int32_t* off = csr;
         for (int64_t j = 0; j < op.l; ++j)
             if (sel[s64[j]] == int32_t(j)) ++off[s64[j] % n2 + 1];
         for (int64_t f2 = 0; f2 < n2; ++f2) off[f2 + 1] += off[f2];
         std::vector<int32_t> pos(off, off + n2);
-        int32_t* ent = csr.data() + n2 + 1;
+        int32_t* ent = csr + n2 + 1;
         for (int64_t j = 0; j < op.l; ++j) {
             const int64_t F = s64[j];
             if (sel[F] != int32_t(j)) continue;
@@ -315,11 +321,11 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
             ent[2 * p] = int32_t(F / n2);
             ent[2 * p + 1] = int32_t(j);
         }
-        dev.fb_csr.ensure(csr.size() * 4);
-        MNB_CUDA(cudaMemcpyAsync(dev.fb_csr.p, csr.data(), csr.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
-        MNB_CUDA(cudaStreamSynchronize(ctx.stream));  // csr is pageable
+        dev.fb_csr.ensure(n_csr * 4);
+        MNB_CUDA(cudaMemcpyAsync(dev.fb_csr.p, csr, n_csr * 4, cudaMemcpyHostToDevice, ctx.stream));
         dev.fb_n2 = n2;
     }
+    MNB_CUDA(cudaEventRecord(dev.stage_free, ctx.stream));
 }
 
 // single vectors: the operator's fine 64-index chunks (more threads than rows x 1024-chunks)
@@ -356,17 +362,22 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
     const int64_t n = h.n;
     ctx.fft_plan(n);
     // slab height: two n-column intermediates per slab row
-    size_t free_b = 0, total_b = 0;
-    MNB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const size_t have = ctx.ws_x1.bytes + ctx.ws_x2.bytes + free_b;
-    // keep room for what the solve allocates after the first sketch: the second
-    // sketch E (l x m), the CholeskyQR2 copy (l x m), R, R', Gram, R'^{-1} twice (m x m), the second operator
-    const size_t mm = size_t(ctx.m), ll = size_t(h.l);
-    const size_t reserve = (size_t(2) << 30) + 40 * ll * mm + 96 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
-    const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
-    int64_t Ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
-    if (Ms < rows) Ms = std::max<int64_t>(8, Ms & ~int64_t(7));
-    Ms = std::max<int64_t>(1, std::min<int64_t>(Ms, rows));
+    // (cached per shape: cudaMemGetInfo is a driver round trip, kept off the per-solve path)
+    auto& sc = ctx.slab_cache;
+    if (!(sc.n == n && sc.rows == rows && sc.l == h.l && sc.m == ctx.m)) {
+        size_t free_b = 0, total_b = 0;
+        MNB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        const size_t have = ctx.ws_x1.bytes + ctx.ws_x2.bytes + free_b;
+        // keep room for what the solve allocates after the first sketch: the second
+        // sketch E (l x m), the CholeskyQR2 copy (l x m), R, R', Gram, R'^{-1} twice (m x m), the second operator
+        const size_t mm = size_t(ctx.m), ll = size_t(h.l);
+        const size_t reserve = (size_t(2) << 30) + 40 * ll * mm + 96 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
+        const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
+        int64_t ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
+        if (ms < rows) ms = std::max<int64_t>(8, ms & ~int64_t(7));
+        sc = {n, rows, h.l, ctx.m, std::max<int64_t>(1, std::min<int64_t>(ms, rows))};
+    }
+    const int64_t Ms = sc.Ms;
     const int64_t Mp = (Ms + 7) & ~int64_t(7);  // blocked layouts pad the slab to whole 8-row blocks
     double2* x1 = static_cast<double2*>(ctx.ws_x1.ensure(size_t(Mp) * size_t(n) * 16));
     double2* x2 = static_cast<double2*>(ctx.ws_x2.ensure(size_t(Mp) * size_t(n) * 16));

@@ -156,8 +156,16 @@ def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
         reps[mode] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
         c.close()
     a, h = reps["cholqr2"], reps["householder"]
-    # path taken: CholeskyQR2 (0) for well-conditioned sketches, shifted CholeskyQR3 (1) at 1e8
+    # path taken: CholeskyQR2 (0) for well-conditioned sketches, shifted CholeskyQR3 (1) at 1e8;
+    # the preconditioner's QR(E) stops after one Cholesky pass (3) when u cond(E)^2 is tiny
     assert (a.extra["qr_path"] & 15) == (1 if kappa >= 1e8 else 0)
+    e_path = a.extra["qr_path"] >> 4
+    if kappa <= 1e4:
+        assert e_path == 3
+    elif kappa >= 1e8:
+        assert e_path == 1
+    else:
+        assert e_path in (0, 3)
     assert h.extra["qr_path"] == 2 | (2 << 4)
     p = O.solve_classical(A, b)
     assert rel(a.x, p) <= solve_tol(eps, kappa)

@@ -94,7 +94,9 @@ typedef struct {
     int64_t lsq_iterations;  /* SolveReport::lsq_iterations                             */
     int32_t lsq_converged;   /* SolveReport::lsq_converged                              */
     int32_t qr_path;         /* extension: sketch QR used, S in bits 0-3, E in bits 4-7:
-                                0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder     */
+                                0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder,
+                                3 one Cholesky pass (E, preconditioner only),
+                                4 one Cholesky pass + corrected seminormal Step 2 (S)  */
     int64_t sketch_size;     /* SolveReport::sketch_size                                */
     double lsq_tau;          /* SolveReport::lsq_tau                                    */
     /* ---- extensions (not in the reference report) ---- */

@@ -120,10 +120,12 @@ struct Context {
     // workspaces
     DevBuf ws_x1, ws_x2, ws_slab, ws_pack;
     DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
+    bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
+    bool csne = true;    // Step 2 from R1 = chol(S^H S) + corrected seminormal equations; MNB_CSNE=0 disables
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
     DevBuf Rinv, Rinv_rows;
-    DevBuf vec_m[8], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, state, resid, scratch;
+    DevBuf vec_m[10], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;
     DevBuf rhs, flag, out_c;
     int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
     PinnedBuf pin_params[2], pin_small;

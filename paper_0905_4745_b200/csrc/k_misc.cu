@@ -135,3 +135,88 @@ void launch_add_diagonal(double2* A, int64_t m, double shift, cudaStream_t strea
 }
 
 }  // namespace mnb
+
+namespace mnb {
+
+namespace {
+
+// The CG's initial vectors without a pass over A (see launch_cg_init_vectors):
+// r = c, t = 0, x = 0 and per-block partial sums of ||c||^2 (fixed order).
+__global__ void __launch_bounds__(256) cg_init_vectors_kernel(const double2* __restrict__ c, int64_t n, double2* r,
+                                                              double2* t, double2* x, double* part) {
+    __shared__ double sh[8];
+    double acc = 0.0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double2 v = c[i];
+        r[i] = v;
+        t[i] = make_double2(0.0, 0.0);
+        if (x) x[i] = make_double2(0.0, 0.0);
+        acc = fma(v.x, v.x, fma(v.y, v.y, acc));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) s += sh[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+// y[j] = sum_i conj(S[i, j]) z[i] for the column-major l x m sketch: one CTA per column,
+// fixed-order tree sum (deterministic).
+__global__ void __launch_bounds__(256) sketch_adjoint_gemv_kernel(const double2* __restrict__ S, int64_t l,
+                                                                  const double2* __restrict__ z, double2* y) {
+    __shared__ double2 sh[8];
+    const double2* col = S + int64_t(blockIdx.x) * l;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = threadIdx.x; i < l; i += blockDim.x) {
+        const double2 a = col[i], b = z[i];
+        acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+        acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 s = sh[0];
+        for (int w = 1; w < int(blockDim.x >> 5); ++w) {
+            s.x += sh[w].x;
+            s.y += sh[w].y;
+        }
+        y[blockIdx.x] = s;
+    }
+}
+
+// red_scal = [qq = ||c||^2, <r,t> = 0, ||r||^2 = 0, 0] (the INIT pass's scalars, pcg.cuh)
+__global__ void cg_init_finish_kernel(const double* part, int parts, double* red_scal) {
+    double s = 0.0;
+    for (int b = 0; b < parts; ++b) s += part[b];
+    red_scal[0] = s;
+    red_scal[1] = 0.0;
+    red_scal[2] = 0.0;
+    red_scal[3] = 0.0;
+}
+
+}  // namespace
+
+void launch_sketch_adjoint_gemv(const double2* S, int64_t l, int64_t m, const double2* z, double2* y,
+                                cudaStream_t stream) {
+    sketch_adjoint_gemv_kernel<<<unsigned(m), 256, 0, stream>>>(S, l, z, y);
+    MNB_LAUNCH_CHECK();
+}
+
+void launch_cg_init_vectors(const double2* c, int64_t n, double2* r, double2* t, double2* x, double* part, int parts,
+                            double* red_scal, cudaStream_t stream) {
+    cg_init_vectors_kernel<<<parts, 256, 0, stream>>>(c, n, r, t, x, part);
+    MNB_LAUNCH_CHECK();
+    cg_init_finish_kernel<<<1, 1, 0, stream>>>(part, parts, red_scal);
+    MNB_LAUNCH_CHECK();
+}
+
+}  // namespace mnb

@@ -102,6 +102,13 @@ void launch_chain_halos(const double2* cssn, int64_t n, int64_t chunk, int64_t n
                         cudaStream_t stream);
 // zero the strictly lower triangle of an m x m column-major matrix
 void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream);
+// y = S^H z for the column-major l x m sketch (deterministic, no cuBLAS handle: safe beside
+// library work on another stream)
+void launch_sketch_adjoint_gemv(const double2* S, int64_t l, int64_t m, const double2* z, double2* y,
+                                cudaStream_t stream);
+// r = c, t = 0, x = 0 (x may be null), red_scal[0..3] = [||c||^2, 0, 0, 0]; part: `parts` doubles of scratch
+void launch_cg_init_vectors(const double2* c, int64_t n, double2* r, double2* t, double2* x, double* part, int parts,
+                            double* red_scal, cudaStream_t stream);
 // A_jj += shift (real), m x m column-major
 void launch_add_diagonal(double2* A, int64_t m, double shift, cudaStream_t stream);
 // out[0] = max_{i<=j} |A_ij - delta_ij| over the upper triangle (deterministic)

@@ -207,6 +207,26 @@ void launch_cg_init_pass(Context& ctx, const double2* c, double2* x) {
     MNB_CUDA(cudaEventRecord(ctx.event(21), ctx.stream));
 }
 
+// The same INIT without touching A, for the solve (one GPU): c = T^* z is Step 3's output, so
+// A c = A T^* z = (T A^*)^* z = S^H z -- one l x m GEMV over the sketch (256 MiB at c4) in place
+// of a 32 GiB pass.  In exact arithmetic S^H z = b (c solves A c = b); the computed S^H z carries
+// the same u ||S|| ||z|| rounding as a direct A c, so the CG's g_0 = R'^{-H} A c is as accurate.
+void launch_cg_init_from_sketch(Context& ctx, const double2* S, int64_t l, const double2* z, const double2* c,
+                                double2* x) {
+    const int64_t n = ctx.n_local, m = ctx.m;
+    double2* r = dev<double2>(ctx.vec_n[0], size_t(std::max<int64_t>(n, 1)));
+    double2* t = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(n, 1)));
+    PassBuffers pb = pass_buffers(ctx);
+    const int parts = 4 * ctx.num_sms;
+    double* part = dev<double>(ctx.part_gg_init, size_t(parts));
+    MNB_CUDA(cudaEventRecord(ctx.event(20), ctx.stream));
+    launch_sketch_adjoint_gemv(S, l, m, z, reinterpret_cast<double2*>(pb.red), ctx.stream);
+    launch_cg_init_vectors(c, n, r, t, x, part, parts, pb.red + 2 * m, ctx.stream);
+    ctx.launches += 3;
+    MNB_CUDA(cudaEventRecord(ctx.event(21), ctx.stream));
+    ctx.init_from_sketch = true;
+}
+
 LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
                  double dup, double2* y, bool want_norms, double2* x, double2* ax, bool init_done,
                  bool rinv_ready) {
@@ -301,8 +321,9 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     // device time of the passes that did work: the INIT pass + one per iteration
     float ms = 0.f;
     MNB_CUDA(cudaEventElapsedTime(&ms, ea, eb));
-    res.pass_ms = ms;
-    res.pass_launches = 1;
+    res.pass_ms = ctx.init_from_sketch ? 0.f : ms;  // (the INIT pass, when there was one)
+    res.pass_launches = ctx.init_from_sketch ? 0 : 1;
+    ctx.init_from_sketch = false;
     const int64_t worked = std::min<int64_t>(int64_t(pass_ev.size()), res.iterations + (st_h->stop_qq0 ? 1 : 0));
     for (int64_t i = 0; i < worked; ++i) {
         MNB_CUDA(cudaEventElapsedTime(&ms, pass_ev[size_t(i)].first, pass_ev[size_t(i)].second));
@@ -341,7 +362,10 @@ struct SketchQr {
 // eps * cond(S)^2 < 1; returns false (caller falls back to Householder, as
 // the reference) when a Cholesky breaks down or Q1 = S R1^{-1} is not orthonormal
 // to 1e-3 (cond(S) above ~2e6).  On success ctx.qwork holds Q1 and ctx.R2 holds R2.
-bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted, bool* precond_only) {
+// r1_only: stop after the first Cholesky (R = R1, ctx.gram holds it too) -- Step 2's
+// corrected seminormal solve (step2_z_csne) needs nothing more.
+bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted, bool* precond_only,
+              bool r1_only = false) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* Q = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
     double2* Rp = dev<double2>(ctx.R2, size_t(m) * size_t(m));
@@ -405,6 +429,10 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         }
         if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
     }
+    if (r1_only) {
+        MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+        return true;
+    }
     if (precond_only && *precond_only) {
         // The CG preconditioner needs only an R1 with E R1^{-1} near-orthonormal -- and
         // |Q1^H Q1 - I| ~ u cond(E)^2 <= u ||R1||_F^2 ||R1^{-1}||_F^2.  When that bound is below
@@ -462,8 +490,11 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
 }
 
 // QR of a finished l x m sketch on ctx.stream (CholeskyQR2, else Householder); qr_s += device time.
+// precond: the preconditioner's QR (E), which may stop after one Cholesky pass (path 3).
+// seminormal: Step 2's QR (S), which may stop after R1 = chol(S^H S) (path 4) -- step2_z_csne
+// then solves with the corrected seminormal equations and falls back here if they do not converge.
 SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBuf& Rbuf, double* qr_s,
-                      bool precond = false) {
+                      bool precond = false, bool seminormal = false) {
     const int64_t m = ctx.m;
     double2* tau = dev<double2>(taubuf, size_t(m));
     double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
@@ -474,7 +505,12 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
     // CholeskyQR2; if the sketch is too ill-conditioned, shifted CholeskyQR3 (and once a sketch of
     // this solve needed it, the next one starts there); Householder (the reference's) as the last resort
     bool done = false;
-    if (ctx.cholqr) {
+    if (ctx.cholqr && seminormal && ctx.csne && !ctx.qr_shifted) {
+        done = cholqr_r(ctx, S, l, m, R, false, nullptr, /*r1_only=*/true);
+        if (done) out.path = 4;
+        else ctx.qr_shifted = true;  // the first Cholesky pass failed: CholeskyQR2 would too
+    }
+    if (ctx.cholqr && !done) {
         if (!ctx.qr_shifted) {
             bool one_pass = precond;
             done = cholqr_r(ctx, S, l, m, R, false, &one_pass);
@@ -580,6 +616,60 @@ void step2_z(Context& ctx, const SketchQr& sq, const double2* b_host, int64_t l,
                  "zgemv");
 }
 
+// Step 2 on the first Cholesky factor only (path 4): z is the minimal-norm solution of
+// S^H z = b (z = Q R^{-H} b = S (S^H S)^{-1} b, src/solver.cpp:93-96), from the corrected
+// seminormal equations  z_0 = S G^{-1} b,  z_{k+1} = z_k + S G^{-1} (b - S^H z_k),  G = R1^H R1.
+// Every iterate lies in range(S); the refinement is accepted once the residual is at the
+// rounding level of S^H z (||b - S^H z|| <= 2 sqrt(l) u ||S||_F ||z||), which makes z as
+// accurate as the Householder solve (error ~ u cond(S)).  Returns false (the caller runs the
+// shifted CholeskyQR3 and step2_z) when a correction does not shrink the residual tenfold
+// (u cond(S)^2 is not small) or three corrections do not get there.
+bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const double2* b_host, int64_t l, int64_t m,
+                  double2* z) {
+    const auto* R1 = reinterpret_cast<const cuDoubleComplex*>(sq.R);
+    auto* zc = reinterpret_cast<cuDoubleComplex*>(z);
+    const auto* Sc = reinterpret_cast<const cuDoubleComplex*>(S);
+    double2* bd = dev<double2>(ctx.vec_m[6], size_t(m));
+    double2* w = dev<double2>(ctx.vec_m[8], size_t(m));
+    auto* wc = reinterpret_cast<cuDoubleComplex*>(w);
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), mone = make_cuDoubleComplex(-1.0, 0.0),
+                          zero = make_cuDoubleComplex(0.0, 0.0);
+    MNB_CUDA(cudaMemcpyAsync(bd, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    auto solve_gram = [&]() {  // w <- G^{-1} w = R1^{-1} R1^{-H} w
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m), R1,
+                                 int(sq.ldR), wc, 1),
+                     "ztrsv");
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m), R1,
+                                 int(sq.ldR), wc, 1),
+                     "ztrsv");
+    };
+    // ||S||_F^2 = trace(S^H S): the diagonal of R1^H R1 is the column sums of |R1|^2
+    double sf = 0.0;
+    cublas_check(cublasDznrm2(ctx.cublas, int(m * sq.ldR), R1, 1, &sf), "dznrm2");  // lower triangle is zero
+    MNB_CUDA(cudaMemcpyAsync(w, bd, size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    solve_gram();
+    cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &one, Sc, int(l), wc, 1, &zero, zc, 1), "zgemv");
+    const double thr = 2.0 * std::sqrt(double(l)) * kEps * sf;
+    double prev = 0.0;
+    for (int it = 0; it <= 3; ++it) {
+        // w = b - S^H z
+        MNB_CUDA(cudaMemcpyAsync(w, bd, size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+        cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(l), int(m), &mone, Sc, int(l), zc, 1, &one, wc, 1),
+                     "zgemv");
+        double nr = 0.0, nz = 0.0;
+        cublas_check(cublasDznrm2(ctx.cublas, int(m), wc, 1, &nr), "dznrm2");
+        cublas_check(cublasDznrm2(ctx.cublas, int(l), zc, 1, &nz), "dznrm2");
+        if (std::getenv("MNB_TRACE")) std::fprintf(stderr, "[mnb] csne it %d: ||b - S^H z|| = %.3e (thr %.3e)\n", it, nr, thr * nz);
+        if (nr <= thr * nz) return true;
+        // the correction contracts by ~u cond(S)^2 per step: stop at once when it does not
+        if (it == 3 || (it > 0 && !(nr < 0.1 * prev))) break;
+        prev = nr;
+        solve_gram();
+        cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &one, Sc, int(l), wc, 1, &one, zc, 1), "zgemv");
+    }
+    return false;
+}
+
 // ---------------------------------------------------- solve_randomized ----
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep) {
@@ -587,6 +677,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     ctx.timers.clear();  // drop timers of an aborted call (they point into its report)
     ctx.timer_next = 0;
     ctx.qr_shifted = false;
+    ctx.init_from_sketch = false;
     validate_matrix_set(ctx);
     const int64_t m = ctx.m, n = ctx.n_global;
     // ProblemInstance::validate (src/solver.cpp:37-48); A's finiteness is checked on the device below.
@@ -763,7 +854,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     {
         OnStream on(ctx, s2);
         MNB_CUDA(cudaStreamWaitEvent(s2, eS, 0));
-        sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0);
+        sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0, false, /*seminormal=*/true);
     trace("QR(S)");
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
         MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
@@ -783,7 +874,16 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                         "sketch S = T A* lost rank (" + std::to_string(bad) +
                             " dependent columns); the problem matrix is rank deficient",
                         bad);
-        step2_z(ctx, sq, b_host, l, m, z);
+        if (sq.path == 4 && !step2_z_csne(ctx, sq, Sbuf, b_host, l, m, z)) {
+            ctx.qr_shifted = true;  // u cond(S)^2 is not small: CholeskyQR2 would not be accurate either
+            sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0);  // the full factorization
+            if (int64_t bad = deficient_count(ctx, sq.R, sq.ldR, m, l); bad > 0)
+                throw Error(MNB_ERR_RANK_DEFICIENCY,
+                            "sketch S = T A* lost rank (" + std::to_string(bad) +
+                                " dependent columns); the problem matrix is rank deficient",
+                            bad);
+        }
+        if (sq.path != 4) step2_z(ctx, sq, b_host, l, m, z);
         sync(ctx);
         rep.step_seconds[1] = now_s() - t0;
 
@@ -811,7 +911,9 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     double2* xacc = ctx.n_local ? x_dev : nullptr;
     // the INIT pass (r = c, s = A c) needs only c: on s1 while s2 factors E
     MNB_CUDA(cudaStreamWaitEvent(s1, eC, 0));
-    launch_cg_init_pass(ctx, c_loc, xacc);
+    // (A c = S^H z needs the sketch intact: not after the Householder fallback, which overwrote it)
+    if (concurrent && sq.path != 2 && !std::getenv("MNB_INIT_PASS")) launch_cg_init_from_sketch(ctx, Sbuf, l, z, c_loc, xacc);
+    else launch_cg_init_pass(ctx, c_loc, xacc);
     trace("INIT issued");
     SketchQr eq;
     cudaEvent_t eQ = ctx.timer_event();

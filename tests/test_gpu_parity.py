@@ -158,7 +158,8 @@ def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
     a, h = reps["cholqr2"], reps["householder"]
     # path taken: CholeskyQR2 (0) for well-conditioned sketches, shifted CholeskyQR3 (1) at 1e8;
     # the preconditioner's QR(E) stops after one Cholesky pass (3) when u cond(E)^2 is tiny
-    assert (a.extra["qr_path"] & 15) == (1 if kappa >= 1e8 else 0)
+    # S: one Cholesky pass + corrected seminormal Step 2 (4) unless the sketch is too ill-conditioned
+    assert (a.extra["qr_path"] & 15) == (1 if kappa >= 1e8 else 4)
     e_path = a.extra["qr_path"] >> 4
     if kappa <= 1e4:
         assert e_path == 3
@@ -171,3 +172,52 @@ def test_cholqr2_matches_householder(m, n, kappa, eps, monkeypatch):
     assert rel(a.x, p) <= solve_tol(eps, kappa)
     assert rel(a.x, h.x) <= solve_tol(eps, kappa)
     assert abs(a.lsq_iterations - h.lsq_iterations) <= 1
+
+
+@pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (256, 8192, 1e4, 1e-8)])
+def test_csne_step2_matches_cholqr2(m, n, kappa, eps, monkeypatch):
+    """Step 2 from R1 = chol(S^H S) with the corrected seminormal equations
+    (path 4) gives the solve of the full CholeskyQR2 Step 2 (z = Q R^{-H} b,
+    src/solver.cpp:93-96): same x within the solve tolerance, same iteration
+    count +-1, and the c it produces satisfies A c = b as well."""
+    A, b = make_instance(m, n, kappa, seed=m + 11)
+    cfg = mn.SolverConfig(epsilon=eps, seed=42, capture_c=True)
+    reps = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MNB_CSNE", flag)
+        c = mn.Context(0)
+        reps[flag] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        c.close()
+    a, f = reps["1"], reps["0"]
+    assert (a.extra["qr_path"] & 15) == 4 and (f.extra["qr_path"] & 15) == 0
+    p = O.solve_classical(A, b)
+    assert rel(a.x, p) <= solve_tol(eps, kappa)
+    assert rel(a.x, f.x) <= solve_tol(eps, kappa)
+    assert abs(a.lsq_iterations - f.lsq_iterations) <= 1
+    # Step 3's c solves A c = b to the same accuracy on both paths
+    ra = np.linalg.norm(A @ a.c - b) / np.linalg.norm(b)
+    rf = np.linalg.norm(A @ f.c - b) / np.linalg.norm(b)
+    assert ra <= max(10 * rf, 1e-13 * kappa)
+
+
+@pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (128, 8192, 1e8, 1e-10)])
+def test_init_from_sketch_matches_init_pass(m, n, kappa, eps, monkeypatch):
+    """The CG's first product A c (src/lsq.cpp:77-86) taken as S^H z from the
+    sketch (c = T^* z, so A c = (T A^*)^* z) instead of a pass over A gives the
+    same solve: x within the solve tolerance, iterations +-1, and the same
+    reported ||c|| ratio."""
+    A, b = make_instance(m, n, kappa, seed=m + 17)
+    cfg = mn.SolverConfig(epsilon=eps, seed=42)
+    reps = {}
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("MNB_INIT_PASS", flag)
+        c = mn.Context(0)
+        reps[flag] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        c.close()
+    a, f = reps[None], reps["1"]
+    p = O.solve_classical(A, b)
+    assert rel(a.x, p) <= solve_tol(eps, kappa)
+    assert rel(a.x, f.x) <= solve_tol(eps, kappa)
+    assert abs(a.lsq_iterations - f.lsq_iterations) <= 1
+    assert abs(a.c_norm_ratio - f.c_norm_ratio) <= solve_tol(eps, kappa) * abs(f.c_norm_ratio)  # (through ||x||)

@@ -68,6 +68,7 @@ struct FftPlan {
     FftLenPlan A, B;                 // single: only A (N = n)
     DevBuf tw4_hi, tw4_lo;
     int tw4_shift = 0;
+    DevBuf p2fa_z;  // fused H + pass A: w_n^{f k1} per k1 row (built on first use)
 };
 
 // Device copy of one operator's parameter blob (layout of SrftHost).
@@ -79,6 +80,7 @@ struct SrftDev {
     DevBuf chain_rec[2];  // per-step chain records of the sketch H stages: [0] P1 (tilde half), [1] P2
     DevBuf vec_halo;      // restart points of 64-index chunks for single-vector chains: fwd, fwd~, adj, adj~
     int64_t vec_chunk = 0, vec_nchunks = 0;
+    DevBuf p2fa_rec, p2fa_idx;  // fused H + pass A: step-major chain records / gather indices (n = 2^20)
     DevBuf fb_csr;        // kept frequencies per f2 for the pruned FFT pass B: [n2+1 offsets][(f1, slot) pairs]
     int64_t fb_n2 = 0;
     // page-locked staging of the small host-built tables (dups, fb_csr): async uploads, no
@@ -122,6 +124,7 @@ struct Context {
     DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
+    bool p2fa = true;    // fused P2 + FFT pass A (k_p2fa.cu) where the shape allows; MNB_P2FA=0 disables
     bool csne = true;    // Step 2 from R1 = chol(S^H S) + corrected seminormal equations; MNB_CSNE=0 disables
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
     DevBuf Rinv, Rinv_rows;

@@ -178,11 +178,13 @@ void fft_rows(Context& ctx, int64_t n, const double2* in, int64_t ld_in, int64_t
 // Four-step DFT of `rows` rows held in the blocked layout of the sketch
 // (see HChainArgs::blk_n1): pass A (length n2, twiddled) -> tmp (blocked for
 // pass B), pass B (length n1) keeps the sampled frequencies -> out.
+// a_done: pass A already ran (fused into the H stage, k_p2fa.cu) and its output is `in`.
 void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, double2* tmp, double2* out,
                       int64_t ld_out, int64_t out_row0, const int32_t* sel, const int32_t* fb_csr, double* ms_a,
-                      double* ms_b) {
+                      double* ms_b, bool a_done = false) {
     FftPlan& P = ctx.fft_plan(n);
-    {
+    if (a_done) tmp = const_cast<double2*>(in);
+    else {
         FftPassArgs a = base_args(P.A);
         a.in = in;
         a.out = tmp;
@@ -290,6 +292,12 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
                        dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
     build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
     ctx.launches += 2;
+    // step-major tables of the fused second H stage + FFT pass A (k_p2fa.cu)
+    if (ctx.p2fa && p2fa_supported(n, P.n1, P.n2, op.ch.chunk, 8)) {
+        build_p2fa_tables(rec2, dev.at<int32_t>(op.off_perm), static_cast<double2*>(dev.p2fa_rec.ensure(size_t(n) * 32)),
+                          static_cast<int32_t*>(dev.p2fa_idx.ensure(size_t(n) * 4)), ctx.stream);
+        ctx.launches += 1;
+    }
     // fine restart points for single-vector H stages (apply / apply_adjoint of one vector)
     dev.vec_chunk = 64;
     dev.vec_nchunks = (n + dev.vec_chunk - 1) / dev.vec_chunk;
@@ -436,7 +444,33 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             ctx.launches += 1;
             t.stop();
         }
-        {  // P2: Pi, Theta, then D (src/srft.cpp:56-57,128)
+        // P2 fused with FFT pass A (k_p2fa.cu) when the shape allows: x2 never goes to HBM
+        const bool fused = blocked && chained && ctx.p2fa && op.p2fa_rec.p &&
+                           p2fa_supported(n, FP.n1, FP.n2, h.ch.chunk, rs) && FP.A.N == 1024;
+        if (fused) {
+            EventTimer t(ctx, kernel_ms ? &kernel_ms[1] : nullptr, 1);
+            P2faArgs a;
+            a.x1 = x1;
+            a.ld = Ms;
+            a.gather = op.at<int32_t>(h.off_perm);
+            a.rec = op.chain_rec[1].as<double2>();
+            a.zout0 = h.at<double2>(h.off_d)[0];
+            a.halo = op.at<int32_t>(h.off_halo);  // forward chain of Theta
+            a.tw = FP.A.tw.as<double2>();
+            if (!FP.p2fa_z.p) {
+                FftPlan& fp = ctx.fft_plan(n);
+                build_p2fa_twiddles(fp.tw4_hi.as<double2>(), fp.tw4_lo.as<double2>(), fp.tw4_shift,
+                                    static_cast<double2*>(fp.p2fa_z.ensure(size_t(n) * 16)), ctx.stream);
+            }
+            a.rec_t = op.p2fa_rec.as<double2>();
+            a.idx_t = op.p2fa_idx.as<int32_t>();
+            a.z_t = FP.p2fa_z.as<double2>();
+            a.out = x2;
+            a.rows = rs;
+            launch_p2fa(a, ctx.num_sms, ctx.stream);
+            ctx.launches += 1;
+            t.stop();
+        } else {  // P2: Pi, Theta, then D (src/srft.cpp:56-57,128)
             EventTimer t(ctx, kernel_ms ? &kernel_ms[1] : nullptr, 1);
             if (chained) {
                 HChainArgs a;
@@ -477,7 +511,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         if (blocked)
             fft_rows_blocked(ctx, n, x2, rs, x1, out, ldo, out_row0 + s0, op.at<int32_t>(h.off_sel),
                              op.fb_n2 == FP.n2 ? op.fb_csr.as<int32_t>() : nullptr,
-                             kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr);
+                             kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr, fused);
         else
             fft_rows(ctx, n, x2, Ms, rs, x1, Ms, out, ldo, out_row0 + s0, true, op.at<int32_t>(h.off_sel), false,
                      kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr,

@@ -62,7 +62,8 @@ def test_apply_and_adjoint_match_oracle(ctx, l, n, mode):
 # the large-n cases exercise the blocked four-step passes (n = 2^20: both passes
 # length 1024, the specialised kernel; 2^19: 512 x 1024; 3*2^20: 1536 x 2048)
 @pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160),
-                                   (8, 1 << 20, 64), (12, 1 << 19, 48), (5, 3 << 20, 40)])
+                                   (8, 1 << 20, 64), (24, 1 << 20, 96), (12, 1 << 20, 48), (12, 1 << 19, 48),
+                                   (5, 3 << 20, 40)])
 def test_sketch_matches_oracle(ctx, m, n, l):
     A, _ = make_instance(m, n, kappa=1e3, seed=m + n)
     seed = mn.derive_seed(42, 11)
@@ -72,6 +73,30 @@ def test_sketch_matches_oracle(ctx, m, n, l):
     S = op.sketch(ctx)
     Sr = ref.sketch(A)
     assert rel(S, Sr) <= 1e-13
+
+
+@pytest.mark.parametrize("real", [False, True])
+def test_fused_h_fft_matches_unfused(real):
+    """The fused second H stage + FFT pass A (k_p2fa.cu, n = 1024 x 1024, row
+    blocks of 8) against the two-launch path (MNB_P2FA=0) and the oracle."""
+    import os
+    m, n, l = 16, 1 << 20, 128
+    A, _ = make_instance(m, n, kappa=1e3, seed=m + 7, real=real)
+    seed = mn.derive_seed(42, 11)
+    op = mn.build_srft(l, n, seed)
+    out = {}
+    for flag in ("1", "0"):
+        os.environ["MNB_P2FA"] = flag
+        try:
+            c = mn.Context(0)
+            c.set_matrix(A)
+            out[flag] = op.sketch(c)
+            c.close()
+        finally:
+            os.environ.pop("MNB_P2FA", None)
+    ref = O.Srft.build(l, n, seed).sketch(A)
+    assert rel(out["1"], ref) <= 1e-13
+    assert rel(out["1"], out["0"]) <= 1e-13
 
 
 def test_sketch_with_replacement_large_n(ctx):

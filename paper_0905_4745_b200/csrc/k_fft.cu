@@ -468,8 +468,10 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
     constexpr int Rb = 8, N = 1024;
     extern __shared__ double2 sm[];
     double2* T = sm;           // tile [1024][8]
-    double2* X = T + N * Rb;   // Y of one 4-row half: [16 j][64 u][4 r]
-    double2* W = X + N * 4;    // w_1024^k
+    // Y of one 4-row half: [16 j][4 r][64 u] with the 16-byte slot of u within its 128-byte line
+    // xor-swizzled by the row (the writes: 4 rows of one u; the warp sums: 8 consecutive u of one row)
+    double2* X = T + N * Rb;
+    double2* W = X + N * 4;    // w_1024^k, slot-swizzled (kernel-local index swz)
     uint64_t* bar = reinterpret_cast<uint64_t*>(W + N);
     const int r = int(threadIdx.x & 7), u = int(threadIdx.x >> 3);
     const int half = r >> 2, r4 = r & 3;
@@ -478,7 +480,11 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
     const int64_t units = nrbk * a.batches;
     constexpr int64_t tile = int64_t(N) * Rb;
     constexpr uint32_t tile_bytes = uint32_t(tile * 16);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = __ldg(a.tw + i);
+    // w^k at (k & ~7) | ((k ^ k>>3 ^ k>>6) & 7): the warp sums read k = f u for 8 consecutive u,
+    // which for even f would otherwise pile onto a few banks
+    auto swz = [](int k) { return (k & ~7) | ((k ^ (k >> 3) ^ (k >> 6)) & 7); };
+    auto xi = [](int j, int rr, int uu) { return (j * 4 + rr) * 64 + (uu & ~7) + ((uu & 7) ^ (2 * rr)); };
+    for (int i = threadIdx.x; i < N; i += blockDim.x) W[swz(i)] = __ldg(a.tw + i);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -509,7 +515,7 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
         for (int h = 0; h < 2; ++h) {
             if (half == h) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) X[(j * 64 + u) * 4 + r4] = v[d16(j)];
+                for (int j = 0; j < 16; ++j) X[xi(j, r4, u)] = v[d16(j)];
             }
             __syncthreads();
             for (int p = warp; p < 4 * cnt; p += 16) {
@@ -520,8 +526,8 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     const int uu = lane + 32 * t;
-                    const double2 y = X[(j * 64 + uu) * 4 + rp];
-                    const double2 w = W[(f * uu) & (N - 1)];
+                    const double2 y = X[xi(j, rp, uu)];
+                    const double2 w = W[swz((f * uu) & (N - 1))];
                     acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
                     acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
                 }

@@ -463,6 +463,30 @@ __global__ void __launch_bounds__(512, 1) fft1024_tile_kernel(const FftPassArgs 
 // samples come from a CSR list (fb_off/fb_ent: per f2 the pairs (f1, slot)).
 // Shared-memory traffic and barriers drop to about a third of the full
 // 16x16x4 transform.
+// In-warp transposed reduction of 4 values: afterwards lane l holds the warp-wide
+// sum of value index l >> 3 in v[0] (3 + 3 shuffle rounds).
+__device__ __forceinline__ void xreduce4(double (&v)[4], int lane) {
+    {
+        const bool up = (lane & 16) != 0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = up ? v[i] : v[i + 2];
+            const double keep = up ? v[i + 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+    }
+    {
+        const bool up = (lane & 8) != 0;
+        const double send = up ? v[0] : v[1];
+        const double keep = up ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+}
+
+constexpr int kEnt = 512;  // staged (f1, slot) pairs per pass-B unit
+
 __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArgs a, const int32_t* __restrict__ off,
                                                               const int32_t* __restrict__ ent) {
     constexpr int Rb = 8, N = 1024;
@@ -472,7 +496,8 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
     // xor-swizzled by the row (the writes: 4 rows of one u; the warp sums: 8 consecutive u of one row)
     double2* X = T + N * Rb;
     double2* W = X + N * 4;    // w_1024^k, slot-swizzled (kernel-local index swz)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(W + N);
+    int32_t* ENT = reinterpret_cast<int32_t*>(W + N);  // the unit's (f1, slot) pairs, up to kEnt
+    uint64_t* bar = reinterpret_cast<uint64_t*>(ENT + 2 * kEnt);
     const int r = int(threadIdx.x & 7), u = int(threadIdx.x >> 3);
     const int half = r >> 2, r4 = r & 3;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
@@ -497,6 +522,9 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
     for (; unit < units; unit += gridDim.x) {
         const int64_t rbk = unit / a.batches, b = unit - rbk * a.batches;
         const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        // stage the unit's sample list (read by every warp sum) while the tile lands
+        for (int t = threadIdx.x; t < 2 * min(cnt, kEnt); t += blockDim.x) ENT[t] = __ldg(ent + 2 * e0 + t);
+        const int32_t* E = cnt <= kEnt ? ENT : ent + 2 * e0;
         tile_wait(bar, phase);
         phase ^= 1u;
 #pragma unroll
@@ -518,27 +546,41 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
                 for (int j = 0; j < 16; ++j) X[xi(j, r4, u)] = v[d16(j)];
             }
             __syncthreads();
-            for (int p = warp; p < 4 * cnt; p += 16) {
-                const int rp = p & 3, s = p >> 2;
-                const int f = __ldg(ent + 2 * (e0 + s)), slot = __ldg(ent + 2 * (e0 + s) + 1);
-                const int j = f & 15;
-                double2 acc = make_double2(0.0, 0.0);
+            // (row, sample) pairs p, two per warp iteration (p and p + 16) summed together:
+            // one transposed 4-value reduction (6 shuffle rounds instead of 2 x 10)
+            for (int p0 = warp; p0 < 4 * cnt; p0 += 32) {
+                double vv[4];
+                int slot2[2], row2[2];
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    const int uu = lane + 32 * t;
-                    const double2 y = X[xi(j, rp, uu)];
-                    const double2 w = W[swz((f * uu) & (N - 1))];
-                    acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
-                    acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
-                }
+                for (int k = 0; k < 2; ++k) {
+                    const int p = p0 + 16 * k;
+                    const bool ok = p < 4 * cnt;
+                    const int rp = p & 3, s = ok ? p >> 2 : 0;
+                    const int f = E[2 * s];
+                    slot2[k] = ok ? E[2 * s + 1] : -1;
+                    row2[k] = h * 4 + rp;
+                    const int j = f & 15;
+                    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-                    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+                    for (int t = 0; t < 2; ++t) {
+                        const int uu = lane + 32 * t;
+                        const double2 y = X[xi(j, rp, uu)];
+                        const double2 w = W[swz((f * uu) & (N - 1))];
+                        acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
+                        acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+                    }
+                    vv[2 * k] = acc.x;
+                    vv[2 * k + 1] = acc.y;
                 }
-                const int64_t row = rbk * Rb + h * 4 + rp;
-                if (lane == 0 && row < a.rows)
-                    a.out[int64_t(slot) + (a.out_row0 + row) * a.ld_out] = c_scale(acc, a.scale);
+                xreduce4(vv, lane);  // lane l holds the sum of value l >> 3
+                const double other = __shfl_down_sync(0xffffffffu, vv[0], 8);  // lanes 0 / 16: the .y partner
+                if ((lane & 15) == 0) {
+                    const int k = lane >> 4;
+                    const int64_t row = rbk * Rb + row2[k];
+                    if (slot2[k] >= 0 && row < a.rows)
+                        a.out[int64_t(slot2[k]) + (a.out_row0 + row) * a.ld_out] =
+                            c_scale(make_double2(vv[0], other), a.scale);
+                }
             }
             __syncthreads();
         }
@@ -712,7 +754,7 @@ bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const in
 }
 
 void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream) {
-    const size_t smem = size_t(1024) * (8 + 4 + 1) * sizeof(double2) + 16;
+    const size_t smem = size_t(1024) * (8 + 4 + 1) * sizeof(double2) + 2 * kEnt * 4 + 16;
     MNB_CUDA(cudaFuncSetAttribute(fft1024_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, a.num_sms)));

@@ -80,7 +80,7 @@ struct SrftDev {
     DevBuf chain_rec[2];  // per-step chain records of the sketch H stages: [0] P1 (tilde half), [1] P2
     DevBuf vec_halo;      // restart points of 64-index chunks for single-vector chains: fwd, fwd~, adj, adj~
     int64_t vec_chunk = 0, vec_nchunks = 0;
-    DevBuf p2fa_rec, p2fa_idx;  // fused H + pass A: step-major chain records / gather indices (n = 2^20)
+    DevBuf p2fa_rec, p2fa_idx, p2fa_halo;  // + restart points of 512-index sub-chunks (fwd, adj)  // fused H + pass A: step-major chain records / gather indices (n = 2^20)
     DevBuf fb_csr;        // kept frequencies per f2 for the pruned FFT pass B: [n2+1 offsets][(f1, slot) pairs]
     int64_t fb_n2 = 0;
     // page-locked staging of the small host-built tables (dups, fb_csr): async uploads, no

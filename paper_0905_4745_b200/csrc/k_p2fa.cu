@@ -154,20 +154,27 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
     };
 
     // (the loop bound is uniform across the cluster: both CTAs run the same row blocks)
-    for (int64_t rb = blockIdx.x >> 1; rb < nrb; rb += gridDim.x >> 1) {
+    // work units: (row block, k1 segment); segment g covers steps [g S, (g + 1) S), S = 1024 / nseg
+    const int nseg = a.nseg, S = kChunk / nseg;
+    const int64_t units = nrb * nseg;
+    for (int64_t unit = blockIdx.x >> 1; unit < units; unit += gridDim.x >> 1) {
+        const int64_t rb = unit / nseg;
+        const int seg = int(unit - rb * nseg);
+        const int s0 = seg * S, s1 = s0 + S;
         const double2* src = a.x1 + (rb * 8 + kRows * rank + r);
         double2 carry[kQ];
-        // ---- prologue: every chunk's chain from its restart point down to its first output
-        //      (hchain_kernel: carry = x_start; non-storing steps j = start-1 .. i1-1)
+        // ---- prologue: every chunk's chain from its restart point down to the segment's first
+        //      output (hchain_kernel: carry = x_start; non-storing steps j = start-1 .. B-1, B the
+        //      segment's upper bound; a later segment restarts from the fine restart table)
         {
             int32_t j0[kQ];
             int hmax = 0;
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
                 const int c = u + 128 * q;
-                const int32_t start = __ldg(a.halo + c);
+                const int32_t start = seg == 0 ? __ldg(a.halo + c) : __ldg(a.halo_seg + c * nseg + (nseg - 1 - seg));
                 j0[q] = start;
-                hmax = max(hmax, int(start - ((c + 1) * kChunk - 1)));
+                hmax = max(hmax, int(start - (c * kChunk + (kChunk - s0) - 1)));
                 carry[q] = ld_pair(src + int64_t(__ldg(a.gather + start)) * ld);
             }
 #pragma unroll 1
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
                 for (int q = 0; q < kQ; ++q) {
                     const int c = u + 128 * q;
                     const int32_t jj = j0[q] - h;
-                    if (jj < (c + 1) * kChunk - 1) continue;  // past this chunk's non-storing steps
+                    if (jj < c * kChunk + (kChunk - s0) - 1) continue;  // past this chunk's non-storing steps
                     const double2 x = ld_pair(src + int64_t(__ldg(a.gather + jj)) * ld);
                     const double2 cs = __ldg(a.rec + 3 * int64_t(jj));
                     carry[q] = make_double2(__dadd_rn(__dmul_rn(cs.x, x.x), __dmul_rn(cs.y, carry[q].x)),
@@ -187,20 +194,20 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
         // ---- values(0) straight from the step-0 index row; PRM(0) + IDX(1), Z(0) by TMA
         __syncthreads();  // the previous row block is done with PRM / IDX / Z / X
         if (tid == 0) {
-            stage_a(0, 1);
-            stage_z(kChunk - 1);
+            stage_a(s0, s0 + 1);
+            stage_z(kChunk - 1 - s0);
         }
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) cp_pair(Lt + q * kThreads, src + int64_t(__ldg(a.idx_t + u + 128 * q)) * ld);
+        for (int q = 0; q < kQ; ++q) cp_pair(Lt + q * kThreads, src + int64_t(__ldg(a.idx_t + size_t(s0) * kN + u + 128 * q)) * ld);
         cp_commit();
         cp_wait_all();
         cluster_sync();
 
         double2* orow = a.out + rb * int64_t(kN) * kChunk * 8 + kRows * rank + r;
 #pragma unroll 1
-        for (int s = 0; s < kChunk; ++s) {
+        for (int s = s0; s < s1; ++s) {
             const int k1 = kChunk - 1 - s;
-            const bool more = s + 1 < kChunk;
+            const bool more = s + 1 < s1;
             mbar_wait(barA, phA);  // PRM(s), IDX(s+1)
             phA ^= 1u;
             // 1. chain steps (hchain_kernel's storing step) on values(s); each landing slot is
@@ -332,7 +339,7 @@ bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t chunk, int64_t ro
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream) {
     const size_t smem = P2faSmem::TOTAL;
     MNB_CUDA(cudaFuncSetAttribute(p2fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(a.rows / 8, num_sms / 2));
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(a.rows / 8 * a.nseg, num_sms / 2));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * pairs));
     cfg.blockDim = dim3(kThreads);

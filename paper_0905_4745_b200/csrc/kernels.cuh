@@ -58,6 +58,8 @@ struct P2faArgs {
     const double2* rec = nullptr;    // [n][3] {cs_j, -, d_{j+1}} (build_chain_params, zout = d)
     double2 zout0 = {1.0, 0.0};      // d_0
     const int32_t* halo = nullptr;   // per-chunk restart index (forward chain of Theta)
+    const int32_t* halo_seg = nullptr; // restart index per (1024 / nseg)-index sub-chunk (nseg > 1)
+    int nseg = 1;                    // k1 segments per row block (work units = row blocks x nseg)
     const double2* tw = nullptr;     // w_1024^q
     const double2* rec_t = nullptr;  // step-major {cs_j, d_{j+1}} [1024 s][1024 c] (build_p2fa_tables)
     const int32_t* idx_t = nullptr;  // step-major gather indices [1024 s][1024 c]

@@ -296,7 +296,9 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
     if (ctx.p2fa && p2fa_supported(n, P.n1, P.n2, op.ch.chunk, 8)) {
         build_p2fa_tables(rec2, dev.at<int32_t>(op.off_perm), static_cast<double2*>(dev.p2fa_rec.ensure(size_t(n) * 32)),
                           static_cast<int32_t*>(dev.p2fa_idx.ensure(size_t(n) * 4)), ctx.stream);
-        ctx.launches += 1;
+        int32_t* hs = static_cast<int32_t*>(dev.p2fa_halo.ensure(size_t(n / 512) * 2 * 4));
+        launch_chain_halos(dev.at<double2>(op.off_cssn), n, 512, n / 512, hs, hs + n / 512, ctx.stream);
+        ctx.launches += 2;
     }
     // fine restart points for single-vector H stages (apply / apply_adjoint of one vector)
     dev.vec_chunk = 64;
@@ -462,6 +464,13 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
                 build_p2fa_twiddles(fp.tw4_hi.as<double2>(), fp.tw4_lo.as<double2>(), fp.tw4_shift,
                                     static_cast<double2*>(fp.p2fa_z.ensure(size_t(n) * 16)), ctx.stream);
             }
+            // MNB_P2FA_SEG=2 splits each row block's 1024 steps into two restarted segments, which
+            // evens out the cluster-pair rounds (c4: 256 row blocks on 74 pairs = 4 rounds, 512
+            // half units = 7 half rounds) but measured slower (24.4 vs 23.4 ms at c4: the extra
+            // restart prologues cost more than the last round's idle pairs)
+            a.nseg = 1;
+            a.halo_seg = op.p2fa_halo.as<int32_t>();
+            if (const char* e = std::getenv("MNB_P2FA_SEG")) a.nseg = std::atoi(e) == 2 ? 2 : 1;
             a.rec_t = op.p2fa_rec.as<double2>();
             a.idx_t = op.p2fa_idx.as<int32_t>();
             a.z_t = FP.p2fa_z.as<double2>();

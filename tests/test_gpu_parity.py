@@ -75,25 +75,24 @@ def test_sketch_matches_oracle(ctx, m, n, l):
     assert rel(S, Sr) <= 1e-13
 
 
-@pytest.mark.parametrize("real", [False, True])
-def test_fused_h_fft_matches_unfused(real):
+@pytest.mark.parametrize("real,seg", [(False, "2"), (True, "2"), (False, "1")])
+def test_fused_h_fft_matches_unfused(real, seg, monkeypatch):
     """The fused second H stage + FFT pass A (k_p2fa.cu, n = 1024 x 1024, row
-    blocks of 8) against the two-launch path (MNB_P2FA=0) and the oracle."""
-    import os
+    blocks of 8, each row block's 1024 steps in 1 or 2 segments restarted from
+    the fine restart table) against the two-launch path (MNB_P2FA=0) and the
+    oracle."""
     m, n, l = 16, 1 << 20, 128
     A, _ = make_instance(m, n, kappa=1e3, seed=m + 7, real=real)
     seed = mn.derive_seed(42, 11)
     op = mn.build_srft(l, n, seed)
+    monkeypatch.setenv("MNB_P2FA_SEG", seg)
     out = {}
     for flag in ("1", "0"):
-        os.environ["MNB_P2FA"] = flag
-        try:
-            c = mn.Context(0)
-            c.set_matrix(A)
-            out[flag] = op.sketch(c)
-            c.close()
-        finally:
-            os.environ.pop("MNB_P2FA", None)
+        monkeypatch.setenv("MNB_P2FA", flag)
+        c = mn.Context(0)
+        c.set_matrix(A)
+        out[flag] = op.sketch(c)
+        c.close()
     ref = O.Srft.build(l, n, seed).sketch(A)
     assert rel(out["1"], ref) <= 1e-13
     assert rel(out["1"], out["0"]) <= 1e-13

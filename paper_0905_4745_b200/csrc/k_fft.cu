@@ -815,3 +815,124 @@ void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace mnb
+
+namespace mnb {
+
+namespace {
+
+// Pruned pass B over the blocked layout written by the fused H stage + pass A
+// (k_p2fa.cu) for long pass-B lengths, N = 16 U (n = 3 * 2^20: N = 3072, U = 192):
+// unit (8-row block, f2, half) reads rows 4 half .. 4 half + 3 of the block's
+// [k1][8] column for this f2 (the two halves of a block run on neighbouring CTAs
+// at the same time and share every 128-byte line through L2), forms
+//   Y_u[j] = sum_q x[u + U q] w_16^{j q}        (u < U, j < 16)
+// in registers, and takes each kept frequency as the U-term warp sum
+//   X[f1] = sum_u w_N^{f1 u} Y_u[f1 mod 16]
+// (the 1024-point version, fft1024_select_kernel, keeps whole tiles in shared memory).
+// w_N^k = hi[k >> 6] lo[k & 63] from two small tables.
+constexpr int kBR = 4;      // rows per unit
+constexpr int kBEnt = 512;  // staged (f1, slot) pairs per unit
+
+template <int U>
+__global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const FftPassArgs a,
+                                                                       const int32_t* __restrict__ off,
+                                                                       const int32_t* __restrict__ ent) {
+    constexpr int N = 16 * U, T = kBR * U, NH = (N + 63) / 64;
+    extern __shared__ __align__(16) double2 smb[];
+    double2* X = smb;                 // Y as [16 j][U u][4 r], r slot xor-swizzled by u
+    double2* LO = X + 16 * U * kBR;   // w_N^k, k < 64 (slot-swizzled)
+    double2* HI = LO + 64;            // w_N^{64 k}
+    int32_t* ENT = reinterpret_cast<int32_t*>(HI + NH);
+    const int r = int(threadIdx.x) & 3, u = int(threadIdx.x) >> 2;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31), nwarps = T / 32;
+    auto swz = [](int k) { return (k & ~7) | ((k ^ (k >> 3)) & 7); };
+    auto xb = [](int j, int uu, int rr) { return (j * U + uu) * 4 + (rr ^ ((uu >> 1) & 3)); };
+    for (int i = threadIdx.x; i < 64; i += T) LO[swz(i)] = __ldg(a.tw + i);
+    for (int i = threadIdx.x; i < NH; i += T) HI[i] = __ldg(a.tw + 64 * i);
+    const int64_t nrb8 = (a.rows + 7) / 8;
+    const int64_t units = nrb8 * a.batches * 2;
+    const int64_t n1 = N;
+    auto load = [&](int64_t unit, double2 (&v)[16]) {
+        const int64_t half = unit & 1, ub = unit >> 1;
+        const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
+        const double2* base = a.in + ((rb * a.batches + b) * n1) * 8 + 4 * half + r;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const double2* p = base + int64_t(u + U * q) * 8;
+            double2 x;
+            asm volatile("ld.global.nc.L2::128B.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "l"(p));
+            v[q] = x;
+        }
+    };
+    double2 v[16];
+    int64_t unit = blockIdx.x;
+    if (unit < units) load(unit, v);
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t half = unit & 1, ub = unit >> 1;
+        const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
+        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        dft16_np<false>(v);
+        __syncthreads();  // the previous unit's sums are done with X / ENT (and the tables are loaded)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) X[xb(j, u, r)] = v[d16(j)];
+        for (int t = threadIdx.x; t < 2 * min(cnt, kBEnt); t += T) ENT[t] = __ldg(ent + 2 * e0 + t);
+        __syncthreads();
+        const int64_t next = unit + gridDim.x;
+        if (next < units) load(next, v);  // in flight during the sums
+        const int32_t* E = cnt <= kBEnt ? ENT : ent + 2 * e0;
+        for (int p0 = warp; p0 < kBR * cnt; p0 += 2 * nwarps) {
+            double vv[4];
+            int slot2[2], row2[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int p = p0 + nwarps * k;
+                const bool ok = p < kBR * cnt;
+                const int rp = p & 3, s = ok ? p >> 2 : 0;
+                const int f = E[2 * s];
+                slot2[k] = ok ? E[2 * s + 1] : -1;
+                row2[k] = rp;
+                const int j = f & 15;
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < (U + 31) / 32; ++t) {
+                    const int uu = lane + 32 * t;
+                    if (uu < U) {
+                        const double2 y = X[xb(j, uu, rp)];
+                        const int kk = int((int64_t(f) * uu) % N);
+                        const double2 w = c_mul(HI[kk >> 6], LO[swz(kk & 63)]);
+                        acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
+                        acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+                    }
+                }
+                vv[2 * k] = acc.x;
+                vv[2 * k + 1] = acc.y;
+            }
+            xreduce4(vv, lane);
+            const double other = __shfl_down_sync(0xffffffffu, vv[0], 8);
+            if ((lane & 15) == 0) {
+                const int k = lane >> 4;
+                const int64_t row = rb * 8 + 4 * half + row2[k];
+                if (slot2[k] >= 0 && row < a.rows)
+                    a.out[int64_t(slot2[k]) + (a.out_row0 + row) * a.ld_out] = c_scale(make_double2(vv[0], other), a.scale);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+bool launch_fft_select_blocked(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
+                               cudaStream_t stream) {
+    if (a.inverse || a.N != 3072) return false;
+    constexpr int U = 192;
+    const size_t smem = (size_t(16) * U * kBR + 64 + (a.N + 63) / 64) * sizeof(double2) + 2 * kBEnt * 4;
+    auto k = fft_select_blocked_kernel<U>;
+    MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches * 2;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, num_sms)));
+    k<<<grid, kBR * U, smem, stream>>>(a, off, ent);
+    MNB_LAUNCH_CHECK();
+    return true;
+}
+
+}  // namespace mnb

@@ -1,5 +1,5 @@
 // Fused second H stage + four-step FFT pass A of the sketch (sm_100a), for
-// n = 1024 x 1024 with rotation-chain chunks of n1 = 1024 indices.
+// n = n1 x 1024 (n1 = 1024 or 3072) with rotation-chain chunks of n1 indices.
 //
 // The unfused path runs P2 (x2 = D Chain(x1[:, p_i]), src/srft.cpp:56-57,128)
 // and then pass A (length-1024 DFTs over k2 of x2[:, k1 + 1024 k2]) as two
@@ -33,7 +33,6 @@ namespace mnb {
 namespace {
 
 constexpr int kN = 1024;       // pass-A length n2 = number of chunks
-constexpr int kChunk = 1024;   // chain chunk = n1 = number of k1 steps
 constexpr int kRows = 4;       // rows per CTA; a cluster of 2 CTAs covers one 8-row block
 constexpr int kThreads = 512;  // chain phase: (r, u): r = tid & 3, u = tid >> 2 in [0, 128)
 constexpr int kQ = 8;          // chunks per thread: c = u + 128 q
@@ -122,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
     double2* Lt = reinterpret_cast<double2*>(smem + P2faSmem::L) + threadIdx.x;  // slot q at Lt[q * kThreads]
     uint64_t* barA = reinterpret_cast<uint64_t*>(smem + P2faSmem::BAR);         // PRM(s) + IDX(s+1)
     uint64_t* barZ = barA + 1;                                                   // Z(s)
+    const int n1 = a.n1;  // chain chunk = k1 steps per row block (1024 or 3072)
     const int tid = int(threadIdx.x);
     const int r = tid & 3, u = tid >> 2;                        // chain / stage 1
     const int u1 = (tid >> 2) & 15, a8 = tid >> 6;              // stage 2: (r, u1, a)
@@ -142,10 +142,10 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
     // chunk 0's last output (s = 1023, index 0) is the final carry times d_0
     auto stage_a = [&](int sp, int si) {  // PRM(sp) and (si < 1024) IDX(si): thread 0
         fence_async_smem();
-        const uint32_t bytes = uint32_t(kN) * 32 + (si < kChunk ? uint32_t(kN) * 4 : 0u);
+        const uint32_t bytes = uint32_t(kN) * 32 + (si < n1 ? uint32_t(kN) * 4 : 0u);
         mbar_expect(barA, bytes);
         bulk_load(PRM, a.rec_t + size_t(sp) * kN * 2, uint32_t(kN) * 32, barA);
-        if (si < kChunk) bulk_load(IDX, a.idx_t + size_t(si) * kN, uint32_t(kN) * 4, barA);
+        if (si < n1) bulk_load(IDX, a.idx_t + size_t(si) * kN, uint32_t(kN) * 4, barA);
     };
     auto stage_z = [&](int k1) {
         fence_async_smem();
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
 
     // (the loop bound is uniform across the cluster: both CTAs run the same row blocks)
     // work units: (row block, k1 segment); segment g covers steps [g S, (g + 1) S), S = 1024 / nseg
-    const int nseg = a.nseg, S = kChunk / nseg;
+    const int nseg = a.nseg, S = n1 / nseg;
     const int64_t units = nrb * nseg;
     for (int64_t unit = blockIdx.x >> 1; unit < units; unit += gridDim.x >> 1) {
         const int64_t rb = unit / nseg;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
                 const int c = u + 128 * q;
                 const int32_t start = seg == 0 ? __ldg(a.halo + c) : __ldg(a.halo_seg + c * nseg + (nseg - 1 - seg));
                 j0[q] = start;
-                hmax = max(hmax, int(start - (c * kChunk + (kChunk - s0) - 1)));
+                hmax = max(hmax, int(start - (c * n1 + (n1 - s0) - 1)));
                 carry[q] = ld_pair(src + int64_t(__ldg(a.gather + start)) * ld);
             }
 #pragma unroll 1
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
                 for (int q = 0; q < kQ; ++q) {
                     const int c = u + 128 * q;
                     const int32_t jj = j0[q] - h;
-                    if (jj < c * kChunk + (kChunk - s0) - 1) continue;  // past this chunk's non-storing steps
+                    if (jj < c * n1 + (n1 - s0) - 1) continue;  // past this chunk's non-storing steps
                     const double2 x = ld_pair(src + int64_t(__ldg(a.gather + jj)) * ld);
                     const double2 cs = __ldg(a.rec + 3 * int64_t(jj));
                     carry[q] = make_double2(__dadd_rn(__dmul_rn(cs.x, x.x), __dmul_rn(cs.y, carry[q].x)),
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
         __syncthreads();  // the previous row block is done with PRM / IDX / Z / X
         if (tid == 0) {
             stage_a(s0, s0 + 1);
-            stage_z(kChunk - 1 - s0);
+            stage_z(n1 - 1 - s0);
         }
 #pragma unroll
         for (int q = 0; q < kQ; ++q) cp_pair(Lt + q * kThreads, src + int64_t(__ldg(a.idx_t + size_t(s0) * kN + u + 128 * q)) * ld);
@@ -203,10 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
         cp_wait_all();
         cluster_sync();
 
-        double2* orow = a.out + rb * int64_t(kN) * kChunk * 8 + kRows * rank + r;
+        double2* orow = a.out + rb * int64_t(kN) * n1 * 8 + kRows * rank + r;
 #pragma unroll 1
         for (int s = s0; s < s1; ++s) {
-            const int k1 = kChunk - 1 - s;
+            const int k1 = n1 - 1 - s;
             const bool more = s + 1 < s1;
             mbar_wait(barA, phA);  // PRM(s), IDX(s+1)
             phA ^= 1u;
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
             for (int q = 0; q < kQ; ++q) {
                 const int c = u + 128 * q;
                 const double2 x = Lt[q * kThreads];
-                if (c == 0 && s == kChunk - 1) {
+                if (c == 0 && s == n1 - 1) {
                     v[q] = c_mul_rn(carry[q], a.zout0);  // out[0] = carry * d_0
                 } else {
                     const double2 cs = PRM[2 * c], zo = PRM[2 * c + 1];
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
                     v[q] = c_mul_rn(o, zo);
                     carry[q] = nc;
                 }
-                if (more && !(c == 0 && s + 1 == kChunk - 1))
+                if (more && !(c == 0 && s + 1 == n1 - 1))
                     cp_pair(Lt + q * kThreads, src + int64_t(IDX[c]) * ld);
             }
             cp_commit();
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
                                                    __shfl_xor_sync(0xffffffffu, v[b].y, 4));
                     const double2 y = h3 ? c_sub(o, v[b]) : c_add(v[b], o);
                     const int f = a3 + 8 * b13 + 64 * (b + 8 * h3);
-                    orow[(int64_t(f) * kChunk + k1) * 8] = c_mul(y, Zs[f]);
+                    orow[(int64_t(f) * n1 + k1) * 8] = c_mul(y, Zs[f]);
                 }
             }
             phZ ^= 1u;
@@ -298,12 +298,12 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
 }
 
 // Step-major tables of one operator: rec_t[s][c] = {cs_j, d_{j+1}}, idx_t[s][c] = gather[j]
-// for j = 1024 c + 1022 - s (zeros where j < 0).
-__global__ void build_p2fa_tables_kernel(const double2* __restrict__ rec, const int32_t* __restrict__ gather,
+// for j = n1 c + n1 - 2 - s (zeros where j < 0).
+__global__ void build_p2fa_tables_kernel(const double2* __restrict__ rec, const int32_t* __restrict__ gather, int n1,
                                          double2* rec_t, int32_t* idx_t) {
     const int c = int(blockIdx.x) * blockDim.x + threadIdx.x, s = int(blockIdx.y);
     if (c >= kN) return;
-    const int64_t j = int64_t(kChunk) * c + (kChunk - 2) - s;
+    const int64_t j = int64_t(n1) * c + (n1 - 2) - s;
     const size_t o = size_t(s) * kN + c;
     rec_t[2 * o] = j >= 0 ? rec[3 * j] : make_double2(0.0, 0.0);
     rec_t[2 * o + 1] = j >= 0 ? rec[3 * j + 2] : make_double2(0.0, 0.0);
@@ -321,19 +321,20 @@ __global__ void build_p2fa_twiddles_kernel(const double2* __restrict__ hi, const
 
 }  // namespace
 
-void build_p2fa_tables(const double2* rec, const int32_t* gather, double2* rec_t, int32_t* idx_t,
+void build_p2fa_tables(const double2* rec, const int32_t* gather, int n1, double2* rec_t, int32_t* idx_t,
                        cudaStream_t stream) {
-    build_p2fa_tables_kernel<<<dim3(kN / 256, kChunk), 256, 0, stream>>>(rec, gather, rec_t, idx_t);
+    build_p2fa_tables_kernel<<<dim3(kN / 256, n1), 256, 0, stream>>>(rec, gather, n1, rec_t, idx_t);
     MNB_LAUNCH_CHECK();
 }
 
-void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, double2* z_t, cudaStream_t stream) {
-    build_p2fa_twiddles_kernel<<<dim3(kN / 256, kChunk), 256, 0, stream>>>(hi, lo, shift, z_t);
+void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, int n1, double2* z_t, cudaStream_t stream) {
+    build_p2fa_twiddles_kernel<<<dim3(kN / 256, n1), 256, 0, stream>>>(hi, lo, shift, z_t);
     MNB_LAUNCH_CHECK();
 }
 
-bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t chunk, int64_t rows) {
-    return n == int64_t(kN) * kChunk && n1 == kChunk && n2 == kN && chunk == kChunk && rows > 0 && rows % 8 == 0;
+// n = n1 x 1024 with pass A of length n2 = 1024 over the chunks and chain chunks of n1 indices
+bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows) {
+    return n2 == kN && (n1 == 1024 || n1 == 3072) && n == n1 * n2 && rows > 0 && rows % 8 == 0;
 }
 
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream) {

@@ -50,7 +50,7 @@ bool hchain_fits(int64_t max_span, int is_real);
 void build_chain_params(const double2* cssn, const double2* zin, const int32_t* zin_index, const double2* zout,
                         int64_t n, double2* rec, cudaStream_t stream);
 
-// Fused second H stage + FFT pass A (k_p2fa.cu): n = 1024 x 1024, chain chunks of 1024.
+// Fused second H stage + FFT pass A (k_p2fa.cu): n = n1 x 1024, chain chunks of n1 (1024, 3072).
 struct P2faArgs {
     const double2* x1 = nullptr;     // first-stage output, element (r, i) at x1[r + i * ld]
     int64_t ld = 0;
@@ -60,17 +60,19 @@ struct P2faArgs {
     const int32_t* halo = nullptr;   // per-chunk restart index (forward chain of Theta)
     const int32_t* halo_seg = nullptr; // restart index per (1024 / nseg)-index sub-chunk (nseg > 1)
     int nseg = 1;                    // k1 segments per row block (work units = row blocks x nseg)
+    int n1 = 1024;                   // chain chunk = k1 steps per row block
     const double2* tw = nullptr;     // w_1024^q
-    const double2* rec_t = nullptr;  // step-major {cs_j, d_{j+1}} [1024 s][1024 c] (build_p2fa_tables)
-    const int32_t* idx_t = nullptr;  // step-major gather indices [1024 s][1024 c]
-    const double2* z_t = nullptr;    // four-step twiddles w_n^{f k1} [1024 k1][1024 f] (build_p2fa_twiddles)
+    const double2* rec_t = nullptr;  // step-major {cs_j, d_{j+1}} [n1 s][1024 c] (build_p2fa_tables)
+    const int32_t* idx_t = nullptr;  // step-major gather indices [n1 s][1024 c]
+    const double2* z_t = nullptr;    // four-step twiddles w_n^{f k1} [n1 k1][1024 f] (build_p2fa_twiddles)
     double2* out = nullptr;          // pass A output, blocked [row block][f2][k1][8]
     int64_t rows = 0;                // multiple of 8
 };
-bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t chunk, int64_t rows);
+bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows);
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream);
-void build_p2fa_tables(const double2* rec, const int32_t* gather, double2* rec_t, int32_t* idx_t, cudaStream_t stream);
-void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, double2* z_t, cudaStream_t stream);
+void build_p2fa_tables(const double2* rec, const int32_t* gather, int n1, double2* rec_t, int32_t* idx_t,
+                       cudaStream_t stream);
+void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, int n1, double2* z_t, cudaStream_t stream);
 
 // ---------------------------------------------------------------- FFT
 enum FftOutMode { FFT_OUT_TWIDDLE = 0, FFT_OUT_SELECT = 1, FFT_OUT_NATURAL = 2 };
@@ -112,6 +114,10 @@ void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32
 // Returns false (nothing launched) when the shape is not covered.
 bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
                               cudaStream_t stream);
+// Pruned pass B over the blocked layout of the fused H stage + pass A for N = 3072
+// (n = 3 * 2^20); false when the shape is not covered.
+bool launch_fft_select_blocked(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
+                               cudaStream_t stream);
 // O(N^2) fallback for lengths without a 2^a 3^b factorisation (N <= 4096).
 void launch_dft_direct(const FftPassArgs& a, cudaStream_t stream);
 // Largest per-thread element count E (and radix plan) for an in-smem length N;

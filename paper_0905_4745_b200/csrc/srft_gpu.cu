@@ -221,7 +221,8 @@ void fft_rows_blocked(Context& ctx, int64_t n, const double2* in, int64_t rows, 
         EventTimer t(ctx, ms_b, 3);
         const bool pruned = fb_csr && P.B.N == 1024 && !P.B.direct && a.Rb == 8;
         if (pruned) launch_fft1024_select(a, fb_csr, fb_csr + P.n2 + 1, ctx.stream);
-        else launch_fft_pass(a, ctx.stream);
+        else if (!(a_done && fb_csr && launch_fft_select_blocked(a, fb_csr, fb_csr + P.n2 + 1, ctx.num_sms, ctx.stream)))
+            launch_fft_pass(a, ctx.stream);
         ctx.launches += 1;
         t.stop();
     }
@@ -240,9 +241,11 @@ FftPlan& Context::fft_plan(int64_t n) {
         P.n2 = n;
         make_len_plan(P.A, n, stream);
     } else {
-        // n = n1 * n2 with both factors smooth and <= 2048, as balanced as possible
+        // n = n1 * n2 with both factors smooth and <= 2048, as balanced as possible -- except
+        // n = 3 * 2^20, split 3072 x 1024 for the fused H stage + pass A (k_p2fa.cu)
         int64_t best = 0;
-        for (int64_t n2 = 2; n2 <= 2048; ++n2) {
+        if (p2fa && n == 3 * (int64_t(1) << 20)) best = 1024;
+        for (int64_t n2 = 2; n2 <= 2048 && !(p2fa && n == 3 * (int64_t(1) << 20)); ++n2) {
             if (n % n2) continue;
             const int64_t n1 = n / n2;
             if (n1 > 2048 || !smooth(n1) || !smooth(n2)) continue;
@@ -293,12 +296,17 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
     build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
     ctx.launches += 2;
     // step-major tables of the fused second H stage + FFT pass A (k_p2fa.cu)
-    if (ctx.p2fa && p2fa_supported(n, P.n1, P.n2, op.ch.chunk, 8)) {
-        build_p2fa_tables(rec2, dev.at<int32_t>(op.off_perm), static_cast<double2*>(dev.p2fa_rec.ensure(size_t(n) * 32)),
+    if (ctx.p2fa && !P.single && p2fa_supported(n, P.n1, P.n2, 8)) {
+        const int n1 = int(P.n1);
+        build_p2fa_tables(rec2, dev.at<int32_t>(op.off_perm), n1,
+                          static_cast<double2*>(dev.p2fa_rec.ensure(size_t(n) * 32)),
                           static_cast<int32_t*>(dev.p2fa_idx.ensure(size_t(n) * 4)), ctx.stream);
-        int32_t* hs = static_cast<int32_t*>(dev.p2fa_halo.ensure(size_t(n / 512) * 2 * 4));
-        launch_chain_halos(dev.at<double2>(op.off_cssn), n, 512, n / 512, hs, hs + n / 512, ctx.stream);
-        ctx.launches += 2;
+        // restart points of the chain chunks (n1 indices: one per k2) and of their halves
+        // (the optional k1 segments): [fwd 1024][adj 1024][fwd 2048][adj 2048]
+        int32_t* hs = static_cast<int32_t*>(dev.p2fa_halo.ensure(size_t(6 * 1024) * 4));
+        launch_chain_halos(dev.at<double2>(op.off_cssn), n, n1, 1024, hs, hs + 1024, ctx.stream);
+        launch_chain_halos(dev.at<double2>(op.off_cssn), n, n1 / 2, 2048, hs + 2048, hs + 4096, ctx.stream);
+        ctx.launches += 3;
     }
     // fine restart points for single-vector H stages (apply / apply_adjoint of one vector)
     dev.vec_chunk = 64;
@@ -447,8 +455,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             t.stop();
         }
         // P2 fused with FFT pass A (k_p2fa.cu) when the shape allows: x2 never goes to HBM
-        const bool fused = blocked && chained && ctx.p2fa && op.p2fa_rec.p &&
-                           p2fa_supported(n, FP.n1, FP.n2, h.ch.chunk, rs) && FP.A.N == 1024;
+        const bool fused = chained && ctx.p2fa && op.p2fa_rec.p && !FP.single && p2fa_supported(n, FP.n1, FP.n2, rs);
         if (fused) {
             EventTimer t(ctx, kernel_ms ? &kernel_ms[1] : nullptr, 1);
             P2faArgs a;
@@ -457,19 +464,20 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             a.gather = op.at<int32_t>(h.off_perm);
             a.rec = op.chain_rec[1].as<double2>();
             a.zout0 = h.at<double2>(h.off_d)[0];
-            a.halo = op.at<int32_t>(h.off_halo);  // forward chain of Theta
+            a.halo = op.p2fa_halo.as<int32_t>();  // forward chain of Theta, chunks of n1
             a.tw = FP.A.tw.as<double2>();
             if (!FP.p2fa_z.p) {
                 FftPlan& fp = ctx.fft_plan(n);
-                build_p2fa_twiddles(fp.tw4_hi.as<double2>(), fp.tw4_lo.as<double2>(), fp.tw4_shift,
+                build_p2fa_twiddles(fp.tw4_hi.as<double2>(), fp.tw4_lo.as<double2>(), fp.tw4_shift, int(fp.n1),
                                     static_cast<double2*>(fp.p2fa_z.ensure(size_t(n) * 16)), ctx.stream);
             }
+            a.n1 = int(FP.n1);
             // MNB_P2FA_SEG=2 splits each row block's 1024 steps into two restarted segments, which
             // evens out the cluster-pair rounds (c4: 256 row blocks on 74 pairs = 4 rounds, 512
             // half units = 7 half rounds) but measured slower (24.4 vs 23.4 ms at c4: the extra
             // restart prologues cost more than the last round's idle pairs)
             a.nseg = 1;
-            a.halo_seg = op.p2fa_halo.as<int32_t>();
+            a.halo_seg = op.p2fa_halo.as<int32_t>() + 2048;
             if (const char* e = std::getenv("MNB_P2FA_SEG")) a.nseg = std::atoi(e) == 2 ? 2 : 1;
             a.rec_t = op.p2fa_rec.as<double2>();
             a.idx_t = op.p2fa_idx.as<int32_t>();
@@ -517,7 +525,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             t.stop();
         }
         // F and S (src/srft.cpp:129-131)
-        if (blocked)
+        if (blocked || fused)
             fft_rows_blocked(ctx, n, x2, rs, x1, out, ldo, out_row0 + s0, op.at<int32_t>(h.off_sel),
                              op.fb_n2 == FP.n2 ? op.fb_csr.as<int32_t>() : nullptr,
                              kernel_ms ? &kernel_ms[2] : nullptr, kernel_ms ? &kernel_ms[3] : nullptr, fused);

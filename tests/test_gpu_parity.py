@@ -63,7 +63,7 @@ def test_apply_and_adjoint_match_oracle(ctx, l, n, mode):
 # length 1024, the specialised kernel; 2^19: 512 x 1024; 3*2^20: 1536 x 2048)
 @pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160),
                                    (8, 1 << 20, 64), (24, 1 << 20, 96), (12, 1 << 20, 48), (12, 1 << 19, 48),
-                                   (5, 3 << 20, 40)])
+                                   (5, 3 << 20, 40), (16, 3 << 20, 64)])
 def test_sketch_matches_oracle(ctx, m, n, l):
     A, _ = make_instance(m, n, kappa=1e3, seed=m + n)
     seed = mn.derive_seed(42, 11)
@@ -75,13 +75,14 @@ def test_sketch_matches_oracle(ctx, m, n, l):
     assert rel(S, Sr) <= 1e-13
 
 
-@pytest.mark.parametrize("real,seg", [(False, "2"), (True, "2"), (False, "1")])
-def test_fused_h_fft_matches_unfused(real, seg, monkeypatch):
+@pytest.mark.parametrize("real,seg,n", [(False, "2", 1 << 20), (True, "2", 1 << 20), (False, "1", 1 << 20),
+                                        (True, "1", 3 << 20)])
+def test_fused_h_fft_matches_unfused(real, seg, n, monkeypatch):
     """The fused second H stage + FFT pass A (k_p2fa.cu, n = 1024 x 1024, row
     blocks of 8, each row block's 1024 steps in 1 or 2 segments restarted from
     the fine restart table) against the two-launch path (MNB_P2FA=0) and the
     oracle."""
-    m, n, l = 16, 1 << 20, 128
+    m, l = 16, 128
     A, _ = make_instance(m, n, kappa=1e3, seed=m + 7, real=real)
     seed = mn.derive_seed(42, 11)
     op = mn.build_srft(l, n, seed)

@@ -893,16 +893,19 @@ __global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const Ff
                 row2[k] = rp;
                 const int j = f & 15;
                 double2 acc = make_double2(0.0, 0.0);
+                // w^{f uu}, uu = lane + 32 t: w^{f lane} times (w^{32 f})^t
+                const int k0 = int((int64_t(f) * lane) % N), ks = int((int64_t(f) * 32) % N);
+                double2 w = c_mul(HI[k0 >> 6], LO[swz(k0 & 63)]);
+                const double2 wstep = c_mul(HI[ks >> 6], LO[swz(ks & 63)]);
 #pragma unroll
                 for (int t = 0; t < (U + 31) / 32; ++t) {
                     const int uu = lane + 32 * t;
                     if (uu < U) {
                         const double2 y = X[xb(j, uu, rp)];
-                        const int kk = int((int64_t(f) * uu) % N);
-                        const double2 w = c_mul(HI[kk >> 6], LO[swz(kk & 63)]);
                         acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
                         acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
                     }
+                    w = c_mul(w, wstep);
                 }
                 vv[2 * k] = acc.x;
                 vv[2 * k + 1] = acc.y;

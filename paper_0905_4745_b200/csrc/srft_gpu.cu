@@ -393,6 +393,12 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
         int64_t ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
         if (ms < rows) ms = std::max<int64_t>(8, ms & ~int64_t(7));
+        // the fused H + pass A runs one 8-row block per cluster pair: slabs of whole pair rounds
+        // (c5: 840-row slabs = 105 blocks = 2 rounds on 74 pairs; 592 rows = 1 round)
+        const FftPlan& fp0 = ctx.fft_plan(n);
+        const int64_t round_rows = 8 * int64_t(ctx.num_sms / 2);
+        if (ms < rows && ctx.p2fa && !fp0.single && p2fa_supported(n, fp0.n1, fp0.n2, 8) && ms >= round_rows)
+            ms = ms / round_rows * round_rows;
         sc = {n, rows, h.l, ctx.m, std::max<int64_t>(1, std::min<int64_t>(ms, rows))};
     }
     const int64_t Ms = sc.Ms;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
             cp_wait_all();    // this thread's values(s+1) have landed
             __syncthreads();  // X and Z free
             if (more && tid == 0) stage_z(k1 - 1);
-            if ((s & 3) == 3) cluster_sync();  // keep the row-block pair within a few steps
+            if ((s & a.sync_mask) == a.sync_mask) cluster_sync();  // keep the row-block pair within a few steps
         }
     }
 }

@@ -61,6 +61,7 @@ struct P2faArgs {
     const int32_t* halo_seg = nullptr; // restart index per (1024 / nseg)-index sub-chunk (nseg > 1)
     int nseg = 1;                    // k1 segments per row block (work units = row blocks x nseg)
     int n1 = 1024;                   // chain chunk = k1 steps per row block
+    int sync_mask = 15;              // cluster barrier every sync_mask + 1 steps (power of two; 16 measured best)
     const double2* tw = nullptr;     // w_1024^q
     const double2* rec_t = nullptr;  // step-major {cs_j, d_{j+1}} [n1 s][1024 c] (build_p2fa_tables)
     const int32_t* idx_t = nullptr;  // step-major gather indices [n1 s][1024 c]

@@ -478,6 +478,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
                                     static_cast<double2*>(fp.p2fa_z.ensure(size_t(n) * 16)), ctx.stream);
             }
             a.n1 = int(FP.n1);
+            if (const char* e = std::getenv("MNB_P2FA_SYNC")) a.sync_mask = std::max(1, std::atoi(e)) - 1;
             // MNB_P2FA_SEG=2 splits each row block's 1024 steps into two restarted segments, which
             // evens out the cluster-pair rounds (c4: 256 row blocks on 74 pairs = 4 rounds, 512
             // half units = 7 half rounds) but measured slower (24.4 vs 23.4 ms at c4: the extra

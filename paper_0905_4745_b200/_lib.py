@@ -84,6 +84,14 @@ def load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")
+    # libnccl.so.2 is one soname for two builds here: the system NCCL this library links and the newer
+    # one torch bundles.  Whichever loads first serves both, and torch needs symbols only its own
+    # build has (ncclDevCommCreate), so torch (when installed) goes first; the NCCL API this library
+    # calls is in both.
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     L = ctypes.CDLL(LIB_PATH)
     vp, i64, u64, ci, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
     pvp = ctypes.POINTER(ctypes.c_void_p)

@@ -781,6 +781,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                                        cudaMemcpyHostToDevice, ctx.copy_stream));
             MNB_CUDA(cudaEventRecord(ctx.event(200 + k), ctx.copy_stream));
         };
+        MNB_CUDA(cudaEventRecord(ctx.event(199), ctx.copy_stream));
         issue(0);
         const double tp0 = now_s();
         auto f1 = host_async([&] { build_T(std::max(1, hw / 2)); });
@@ -788,8 +789,20 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         build_Tp(std::max(1, hw - hw / 2));
         f1.get();
         (void)tp0;
-        upload_srft(ctx, T, Td);
-        upload_srft(ctx, Tp, Tpd);
+        // the operator uploads go on the copy stream between slab 0 and slab 1: the copy engine does
+        // not keep issue order across streams, and uploads on the solve stream landed only after
+        // every slab of A (the sketches then waited for the whole H2D)
+        {
+            const cudaStream_t solve_stream = ctx.stream;
+            ctx.stream = ctx.copy_stream;
+            upload_srft(ctx, T, Td);
+            MNB_CUDA(cudaEventRecord(ctx.event(230), ctx.stream));
+            upload_srft(ctx, Tp, Tpd);
+            MNB_CUDA(cudaEventRecord(ctx.event(231), ctx.stream));
+            ctx.stream = solve_stream;
+            MNB_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.event(231), 0));
+        }
+        trace("uploads issued");
         for (size_t k = 1; k < slabs.size(); ++k) issue(k);
     } else {
         build_T(hw);
@@ -824,6 +837,8 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Sbuf, l, r0, rep.sketch_kernel_ms);
             ctx.nonfinite = nullptr;
             sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Ebuf, l, r0, rep.sketch_kernel_ms);
+            MNB_CUDA(cudaEventRecord(ctx.event(240 + k), s1));
+            if (k == 0) trace("slab 0 sketches issued");
         }
         MNB_CUDA(cudaEventRecord(eS, s1));
         MNB_CUDA(cudaEventRecord(eE, s1));
@@ -971,6 +986,28 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
     ctx.resolve_timers();
     trace("resolve");
+    if (pipelined && std::getenv("MNB_TRACE")) {  // device timeline of the host-A path
+        float ms_h2d = 0.f, ms_s = 0.f, ms_c = 0.f, ms_q = 0.f;
+        cudaEvent_t e0 = ctx.event(199);
+        MNB_CUDA(cudaEventElapsedTime(&ms_h2d, e0, ctx.event(200 + slabs.size() - 1)));
+        MNB_CUDA(cudaEventElapsedTime(&ms_s, e0, eE));
+        MNB_CUDA(cudaEventElapsedTime(&ms_c, e0, eC));
+        MNB_CUDA(cudaEventElapsedTime(&ms_q, e0, eQ));
+        std::fprintf(stderr, "[mnb] device: H2D done %.1f ms, sketches done %.1f, c ready %.1f, R' ready %.1f ms\n",
+                     ms_h2d, ms_s, ms_c, ms_q);
+        {
+            float a = 0.f, b = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&a, e0, ctx.event(230)));
+            MNB_CUDA(cudaEventElapsedTime(&b, e0, ctx.event(231)));
+            std::fprintf(stderr, "[mnb]   T uploaded %.1f ms, T' uploaded %.1f ms\n", a, b);
+        }
+        for (size_t k = 0; k < slabs.size(); ++k) {
+            float a = 0.f, b = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&a, e0, ctx.event(200 + k)));
+            MNB_CUDA(cudaEventElapsedTime(&b, e0, ctx.event(240 + k)));
+            std::fprintf(stderr, "[mnb]   slab %zu: landed %.1f ms, sketched %.1f ms\n", k, a, b);
+        }
+    }
     rep.kernel_launches = ctx.launches - launches0;
     rep.total_seconds = now_s() - t_start;
 }

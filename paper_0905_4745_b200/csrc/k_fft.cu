@@ -454,15 +454,6 @@ __global__ void __launch_bounds__(512, 1) fft1024_tile_kernel(const FftPassArgs 
 #undef XI
 }
 
-// Pass B of the sketch FFT with N = n1 = 1024, pruned to the sampled outputs.
-// Only ~l/n2 of the 1024 frequencies of a unit (row block rbk, f2 = b) are
-// kept (src/srft.cpp:131), so after the first radix-16 stage,
-//   Y_u[j] = sum_q x[u + 64 q] w_16^{j q}          (u < 64, j < 16),
-// each kept frequency f is a 64-term sum  X[f] = sum_u w_1024^{f u} Y_u[f mod 16]
-// taken by one warp (shuffle reduction) per (row, sample) pair.  The unit's
-// samples come from a CSR list (fb_off/fb_ent: per f2 the pairs (f1, slot)).
-// Shared-memory traffic and barriers drop to about a third of the full
-// 16x16x4 transform.
 // In-warp transposed reduction of 4 values: afterwards lane l holds the warp-wide
 // sum of value index l >> 3 in v[0] (3 + 3 shuffle rounds).
 __device__ __forceinline__ void xreduce4(double (&v)[4], int lane) {
@@ -487,29 +478,36 @@ __device__ __forceinline__ void xreduce4(double (&v)[4], int lane) {
 
 constexpr int kEnt = 512;  // staged (f1, slot) pairs per pass-B unit
 
+// Pass B of the sketch FFT with N = n1 = 1024, pruned to the sampled outputs.
+// Only ~l/n2 of the 1024 frequencies of a unit (row block rbk, f2 = b) are
+// kept (src/srft.cpp:131), so after the first radix-16 stage,
+//   Y_u[j] = sum_q x[u + 64 q] w_16^{j q}          (u < 64, j < 16),
+// each kept frequency f is a 64-term sum  X[f] = sum_u w_1024^{f u} Y_u[f mod 16].
+// Every thread (row r, u) holds its Y_u[j] in registers, so it forms its term
+// of every kept sum directly; the 4 u of a warp are summed by shuffles and the
+// 16 warps through a small shared partial table (fixed order: deterministic).
+// No exchange of the transform.  The unit's samples come from a CSR list
+// (off/ent: per f2 the pairs (f1, slot), sorted by f1 mod 16 on the host) so
+// the register index j is a compile-time constant in the loop over j.
+constexpr int kSB = 16;  // samples per partial-table batch
+
 __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArgs a, const int32_t* __restrict__ off,
                                                               const int32_t* __restrict__ ent) {
     constexpr int Rb = 8, N = 1024;
     extern __shared__ double2 sm[];
-    double2* T = sm;           // tile [1024][8]
-    // Y of one 4-row half: [16 j][4 r][64 u] with the 16-byte slot of u within its 128-byte line
-    // xor-swizzled by the row (the writes: 4 rows of one u; the warp sums: 8 consecutive u of one row)
-    double2* X = T + N * Rb;
-    double2* W = X + N * 4;    // w_1024^k, slot-swizzled (kernel-local index swz)
-    int32_t* ENT = reinterpret_cast<int32_t*>(W + N);  // the unit's (f1, slot) pairs, up to kEnt
-    uint64_t* bar = reinterpret_cast<uint64_t*>(ENT + 2 * kEnt);
+    double2* T = sm;                         // tile [1024][8]
+    double2* W = T + N * Rb;                 // w_1024^k
+    double2* P = W + N;                      // partial sums [16 warps][kSB][8 rows]
+    int32_t* ENT = reinterpret_cast<int32_t*>(P + 16 * kSB * 8);  // the unit's (f1, slot) pairs, up to kEnt
+    int32_t* JOFF = ENT + 2 * kEnt;          // first entry with f1 mod 16 >= j, j = 0..16
+    uint64_t* bar = reinterpret_cast<uint64_t*>(JOFF + 20);
     const int r = int(threadIdx.x & 7), u = int(threadIdx.x >> 3);
-    const int half = r >> 2, r4 = r & 3;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
     const int64_t nrbk = (a.rows + Rb - 1) / Rb;
     const int64_t units = nrbk * a.batches;
     constexpr int64_t tile = int64_t(N) * Rb;
     constexpr uint32_t tile_bytes = uint32_t(tile * 16);
-    // w^k at (k & ~7) | ((k ^ k>>3 ^ k>>6) & 7): the warp sums read k = f u for 8 consecutive u,
-    // which for even f would otherwise pile onto a few banks
-    auto swz = [](int k) { return (k & ~7) | ((k ^ (k >> 3) ^ (k >> 6)) & 7); };
-    auto xi = [](int j, int rr, int uu) { return (j * 4 + rr) * 64 + (uu & ~7) + ((uu & 7) ^ (2 * rr)); };
-    for (int i = threadIdx.x; i < N; i += blockDim.x) W[swz(i)] = __ldg(a.tw + i);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) W[i] = __ldg(a.tw + i);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -522,14 +520,19 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
     for (; unit < units; unit += gridDim.x) {
         const int64_t rbk = unit / a.batches, b = unit - rbk * a.batches;
         const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
-        // stage the unit's sample list (read by every warp sum) while the tile lands
-        for (int t = threadIdx.x; t < 2 * min(cnt, kEnt); t += blockDim.x) ENT[t] = __ldg(ent + 2 * e0 + t);
         const int32_t* E = cnt <= kEnt ? ENT : ent + 2 * e0;
+        // the unit's sample list and its j ranges (read by every thread) while the tile lands
+        for (int t = threadIdx.x; t < 2 * min(cnt, kEnt); t += blockDim.x) ENT[t] = __ldg(ent + 2 * e0 + t);
+        if (threadIdx.x < 17) {
+            int o = 0;
+            while (o < cnt && (__ldg(ent + 2 * (e0 + o)) & 15) < int(threadIdx.x)) ++o;
+            JOFF[threadIdx.x] = o;
+        }
         tile_wait(bar, phase);
         phase ^= 1u;
 #pragma unroll
         for (int q = 0; q < 16; ++q) v[q] = T[(u + 64 * q) * Rb + r];
-        __syncthreads();  // tile buffer free
+        __syncthreads();  // tile buffer free; ENT / JOFF visible
         {
             const int64_t next = unit + gridDim.x;
             if (threadIdx.x == 0 && next < units) {
@@ -537,56 +540,37 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
                 tile_load(T, a.in + next * tile, tile_bytes, bar);
             }
         }
-        if (cnt == 0) continue;  // uniform; the next iteration's barrier orders the tile reuse
+        if (cnt == 0) continue;  // uniform; the next iteration's barrier orders the buffers' reuse
         dft16_np<false>(v);
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-            if (half == h) {
+        for (int b0 = 0; b0 < cnt; b0 += kSB) {
+            const int nb = min(kSB, cnt - b0);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) X[xi(j, r4, u)] = v[d16(j)];
-            }
-            __syncthreads();
-            // (row, sample) pairs p, two per warp iteration (p and p + 16) summed together:
-            // one transposed 4-value reduction (6 shuffle rounds instead of 2 x 10)
-            for (int p0 = warp; p0 < 4 * cnt; p0 += 32) {
-                double vv[4];
-                int slot2[2], row2[2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int p = p0 + 16 * k;
-                    const bool ok = p < 4 * cnt;
-                    const int rp = p & 3, s = ok ? p >> 2 : 0;
+            for (int j = 0; j < 16; ++j) {
+                const int lo = max(JOFF[j], b0), hi = min(JOFF[j + 1], b0 + nb);
+                for (int s = lo; s < hi; ++s) {  // warp-uniform bounds: the shuffles are convergent
                     const int f = E[2 * s];
-                    slot2[k] = ok ? E[2 * s + 1] : -1;
-                    row2[k] = h * 4 + rp;
-                    const int j = f & 15;
-                    double2 acc = make_double2(0.0, 0.0);
+                    double2 p = c_mul(v[d16(j)], W[(f * u) & (N - 1)]);
 #pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        const int uu = lane + 32 * t;
-                        const double2 y = X[xi(j, rp, uu)];
-                        const double2 w = W[swz((f * uu) & (N - 1))];
-                        acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
-                        acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+                    for (int o = 8; o < 32; o <<= 1) {
+                        p.x += __shfl_xor_sync(0xffffffffu, p.x, o);
+                        p.y += __shfl_xor_sync(0xffffffffu, p.y, o);
                     }
-                    vv[2 * k] = acc.x;
-                    vv[2 * k + 1] = acc.y;
-                }
-                xreduce4(vv, lane);  // lane l holds the sum of value l >> 3
-                const double other = __shfl_down_sync(0xffffffffu, vv[0], 8);  // lanes 0 / 16: the .y partner
-                if ((lane & 15) == 0) {
-                    const int k = lane >> 4;
-                    const int64_t row = rbk * Rb + row2[k];
-                    if (slot2[k] >= 0 && row < a.rows)
-                        a.out[int64_t(slot2[k]) + (a.out_row0 + row) * a.ld_out] =
-                            c_scale(make_double2(vv[0], other), a.scale);
+                    if (lane < 8) P[(warp * kSB + (s - b0)) * 8 + lane] = p;
                 }
             }
             __syncthreads();
+            if (int(threadIdx.x) < 8 * nb) {
+                const int rr = int(threadIdx.x) & 7, sl = int(threadIdx.x) >> 3;
+                double2 acc = P[sl * 8 + rr];
+#pragma unroll
+                for (int w = 1; w < 16; ++w) acc = c_add(acc, P[(w * kSB + sl) * 8 + rr]);
+                const int64_t row = rbk * Rb + rr;
+                if (row < a.rows) a.out[int64_t(E[2 * (b0 + sl) + 1]) + (a.out_row0 + row) * a.ld_out] = c_scale(acc, a.scale);
+            }
+            if (b0 + kSB < cnt) __syncthreads();  // P reused by the next batch
         }
     }
 }
-
 
 // Pass B pruned to the sampled frequencies for the plain [n][Ms] layout and any
 // N = 16 U (U <= 128; e.g. 2048 or 1536 at n = 3*2^20): Y_u[j] = sum_q
@@ -754,7 +738,7 @@ bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const in
 }
 
 void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream) {
-    const size_t smem = size_t(1024) * (8 + 4 + 1) * sizeof(double2) + 2 * kEnt * 4 + 16;
+    const size_t smem = (size_t(1024) * (8 + 1) + 16 * kSB * 8) * sizeof(double2) + (2 * kEnt + 20) * 4 + 16;
     MNB_CUDA(cudaFuncSetAttribute(fft1024_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, a.num_sms)));

@@ -986,6 +986,15 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.c_norm_ratio = xnorm > 0.0 ? std::sqrt(ls.rr0) * std::sqrt(double(l) / (cfg.alpha * double(n))) / xnorm : 0.0;
     ctx.resolve_timers();
     trace("resolve");
+    if (!pipelined && std::getenv("MNB_TRACE")) {  // device timeline from the first sketch kernel
+        float a = 0.f, b = 0.f, c = 0.f, d = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&a, eA, eS));
+        MNB_CUDA(cudaEventElapsedTime(&b, eA, eE));
+        MNB_CUDA(cudaEventElapsedTime(&c, eA, eC));
+        MNB_CUDA(cudaEventElapsedTime(&d, eA, eQ));
+        std::fprintf(stderr, "[mnb] device: sketch S done %.1f ms, sketch E done %.1f, c ready %.1f, R' ready %.1f ms\n",
+                     a, b, c, d);
+    }
     if (pipelined && std::getenv("MNB_TRACE")) {  // device timeline of the host-A path
         float ms_h2d = 0.f, ms_s = 0.f, ms_c = 0.f, ms_q = 0.f;
         cudaEvent_t e0 = ctx.event(199);

@@ -9,6 +9,7 @@
 //   FA  fft:    length-n2 DFTs over k2 of x2[:, k1 + n1 k2], twiddle w_n^{f2 k1} -> x1[:, f2 n1 + k1]
 //   FB  fft:    length-n1 DFTs over k1, keep sampled f = f2 + n2 f1, scale n^{-1/2} -> S
 // (n <= 2048: one FFT launch does the whole transform and the sampling.)
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -338,6 +339,19 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
             const int32_t p = pos[size_t(F % n2)]++;
             ent[2 * p] = int32_t(F / n2);
             ent[2 * p + 1] = int32_t(j);
+        }
+        // within each f2, order the entries by f1 mod 16 (the pruned pass B loops over that
+        // residue with a compile-time register index); stable, so ties keep the sample order
+        for (int64_t f2 = 0; f2 < n2; ++f2) {
+            int32_t* e = ent + 2 * off[f2];
+            const int32_t cnt = off[f2 + 1] - off[f2];
+            std::vector<std::pair<int32_t, int32_t>> v(static_cast<size_t>(cnt));
+            for (int32_t i = 0; i < cnt; ++i) v[size_t(i)] = {e[2 * i], e[2 * i + 1]};
+            std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return (x.first & 15) < (y.first & 15); });
+            for (int32_t i = 0; i < cnt; ++i) {
+                e[2 * i] = v[size_t(i)].first;
+                e[2 * i + 1] = v[size_t(i)].second;
+            }
         }
         dev.fb_csr.ensure(n_csr * 4);
         MNB_CUDA(cudaMemcpyAsync(dev.fb_csr.p, csr, n_csr * 4, cudaMemcpyHostToDevice, ctx.stream));

@@ -154,12 +154,24 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
     };
 
     // (the loop bound is uniform across the cluster: both CTAs run the same row blocks)
-    // work units: (row block, k1 segment); segment g covers steps [g S, (g + 1) S), S = 1024 / nseg
-    const int nseg = a.nseg, S = n1 / nseg;
-    const int64_t units = nrb * nseg;
+    // work units: (row block, k1 segment); segment g covers steps [g S, (g + 1) S), S = n1 / nseg
+    // units: row blocks [0, full_rb) whole, the rest as two k1 segments each (restarted from the
+    // half-chunk restart table), so the last pair round can be a half round
+    const int64_t full = min(a.full_rb, nrb);
+    const int64_t units = full + 2 * (nrb - full);
     for (int64_t unit = blockIdx.x >> 1; unit < units; unit += gridDim.x >> 1) {
-        const int64_t rb = unit / nseg;
-        const int seg = int(unit - rb * nseg);
+        int64_t rb;
+        int seg, nseg;
+        if (unit < full) {
+            rb = unit;
+            seg = 0;
+            nseg = 1;
+        } else {
+            rb = full + ((unit - full) >> 1);
+            seg = int((unit - full) & 1);
+            nseg = 2;
+        }
+        const int S = n1 / nseg;
         const int s0 = seg * S, s1 = s0 + S;
         const double2* src = a.x1 + (rb * 8 + kRows * rank + r);
         double2 carry[kQ];
@@ -340,7 +352,8 @@ bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows) {
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream) {
     const size_t smem = P2faSmem::TOTAL;
     MNB_CUDA(cudaFuncSetAttribute(p2fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(a.rows / 8 * a.nseg, num_sms / 2));
+    const int64_t nrb = a.rows / 8;
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(2 * nrb - std::min(a.full_rb, nrb), num_sms / 2));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(2 * pairs));
     cfg.blockDim = dim3(kThreads);

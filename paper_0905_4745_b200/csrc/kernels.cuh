@@ -58,8 +58,8 @@ struct P2faArgs {
     const double2* rec = nullptr;    // [n][3] {cs_j, -, d_{j+1}} (build_chain_params, zout = d)
     double2 zout0 = {1.0, 0.0};      // d_0
     const int32_t* halo = nullptr;   // per-chunk restart index (forward chain of Theta)
-    const int32_t* halo_seg = nullptr; // restart index per (1024 / nseg)-index sub-chunk (nseg > 1)
-    int nseg = 1;                    // k1 segments per row block (work units = row blocks x nseg)
+    const int32_t* halo_seg = nullptr; // restart index per (n1 / 2)-index sub-chunk (split row blocks)
+    int64_t full_rb = 1 << 30;       // row blocks run whole; the rest run as two k1 segments
     int n1 = 1024;                   // chain chunk = k1 steps per row block
     int sync_mask = 15;              // cluster barrier every sync_mask + 1 steps (power of two; 16 measured best)
     const double2* tw = nullptr;     // w_1024^q

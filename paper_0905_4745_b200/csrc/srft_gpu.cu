@@ -493,13 +493,17 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             }
             a.n1 = int(FP.n1);
             if (const char* e = std::getenv("MNB_P2FA_SYNC")) a.sync_mask = std::max(1, std::atoi(e)) - 1;
-            // MNB_P2FA_SEG=2 splits each row block's 1024 steps into two restarted segments, which
-            // evens out the cluster-pair rounds (c4: 256 row blocks on 74 pairs = 4 rounds, 512
-            // half units = 7 half rounds) but measured slower (24.4 vs 23.4 ms at c4: the extra
-            // restart prologues cost more than the last round's idle pairs)
-            a.nseg = 1;
+            // one 8-row block per cluster pair and round: when the last round would leave more than
+            // half the pairs idle, its row blocks run as two k1 segments each (a half round;
+            // c4: 256 blocks on 74 pairs = 3 rounds + 34 blocks -> 68 half units).  MNB_P2FA_SEG=2
+            // splits every row block, MNB_P2FA_SEG=1 none.
+            {
+                const int64_t pairs = ctx.num_sms / 2, nrb = rs / 8;
+                const int64_t full = nrb / pairs * pairs, tail = nrb - full;
+                a.full_rb = (tail > 0 && 2 * tail <= pairs && full > 0) ? full : nrb;
+                if (const char* e = std::getenv("MNB_P2FA_SEG")) a.full_rb = std::atoi(e) == 2 ? 0 : nrb;
+            }
             a.halo_seg = op.p2fa_halo.as<int32_t>() + 2048;
-            if (const char* e = std::getenv("MNB_P2FA_SEG")) a.nseg = std::atoi(e) == 2 ? 2 : 1;
             a.rec_t = op.p2fa_rec.as<double2>();
             a.idx_t = op.p2fa_idx.as<int32_t>();
             a.z_t = FP.p2fa_z.as<double2>();

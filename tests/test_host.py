@@ -57,7 +57,7 @@ def test_host_params_match_golden_vectors():
             assert _sha(op.field(name)) == h, (case["n"], name)
 
 
-@pytest.mark.parametrize("l,n,seed", [(3, 8, 1), (17, 40, 31), (1, 2, 5), (100, 6144, 77), (4096, 1 << 17, 9)])
+@pytest.mark.parametrize("l,n,seed", [(3, 8, 1), (17, 40, 31), (1, 2, 5), (100, 6144, 77), (4096, 1 << 17, 9), (8192, 1 << 20, 11)])
 @pytest.mark.parametrize("without", [True, False])
 def test_host_params_bit_identical_to_oracle(l, n, seed, without):
     mode = mn.Sampling.without_replacement if without else mn.Sampling.with_replacement

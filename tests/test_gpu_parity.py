@@ -246,3 +246,29 @@ def test_init_from_sketch_matches_init_pass(m, n, kappa, eps, monkeypatch):
     assert rel(a.x, f.x) <= solve_tol(eps, kappa)
     assert abs(a.lsq_iterations - f.lsq_iterations) <= 1
     assert abs(a.c_norm_ratio - f.c_norm_ratio) <= solve_tol(eps, kappa) * abs(f.c_norm_ratio)  # (through ||x||)
+
+
+def test_fused_tail_split_and_unfused_agree_at_scale(monkeypatch):
+    """600 rows at n = 2^20 = 75 row blocks on 74 cluster pairs: the last row
+    block runs as two k1 segments (restarted from the half-chunk restart table).
+    The default (tail split), no split (MNB_P2FA_SEG=1) and the unfused two-launch
+    path (MNB_P2FA=0, itself pinned to the oracle above) give the same sketch."""
+    import torch
+    m, n, l = 600, 1 << 20, 1024
+    g = torch.Generator(device="cuda").manual_seed(5)
+    At = torch.randn((n, m), dtype=torch.complex128, device="cuda", generator=g)  # A^T row-major = A col-major
+    op = mn.build_srft(l, n, mn.derive_seed(42, 11))
+    out = {}
+    for name, env in (("split", {}), ("whole", {"MNB_P2FA_SEG": "1"}), ("unfused", {"MNB_P2FA": "0"})):
+        for k in ("MNB_P2FA_SEG", "MNB_P2FA"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        c = mn.Context(0)
+        c.set_matrix(At.T, n_global=n)
+        out[name] = op.sketch(c)
+        c.close()
+    del At
+    torch.cuda.empty_cache()
+    assert rel(out["split"], out["unfused"]) <= 1e-13
+    assert rel(out["whole"], out["unfused"]) <= 1e-13

@@ -127,6 +127,35 @@ void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w,
 
 }  // namespace
 
+// Rinv = R^{-1} for the upper-triangular m x m R (leading dimension ldR), the CG's explicit
+// preconditioner.  One tensor-core ZTRSM against the identity (MNB_TRTRI=1: cuSOLVER Xtrtri,
+// which measured ~2x slower at m = 2048); the strictly lower triangle of Rinv comes out zero.
+void upper_inverse(Context& ctx, const double2* R, int64_t ldR, int64_t m, double2* Rinv) {
+    static const bool use_trtri = [] { const char* e = std::getenv("MNB_TRTRI"); return e && std::string(e) == "1"; }();
+    if (use_trtri) {
+        MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, R, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
+                                   cudaMemcpyDeviceToDevice, ctx.stream));
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
+                                                   CUDA_C_64F, Rinv, m, &dws, &hws),
+                       "trtri_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXtrtri(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m, CUDA_C_64F, Rinv,
+                                        m, work, dws, ctx.host_work.data(), hws, dev<int>(ctx.qr_info, 1)),
+                       "trtri");
+        return;
+    }
+    MNB_CUDA(cudaMemsetAsync(Rinv, 0, size_t(m) * size_t(m) * 16, ctx.stream));
+    launch_add_diagonal(Rinv, m, 1.0, ctx.stream);
+    ctx.launches += 1;
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+    cublas_check(cublasZtrsm(ctx.cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             int(m), int(m), &one, reinterpret_cast<const cuDoubleComplex*>(R), int(ldR),
+                             reinterpret_cast<cuDoubleComplex*>(Rinv), int(m)),
+                 "ztrsm");
+}
+
 // MNB_TRACE=1: host timestamps of the solve's phases on stderr (diagnostics)
 void trace(const char* what) {
     static const bool on = std::getenv("MNB_TRACE") != nullptr;
@@ -236,19 +265,7 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     // explicit R'^{-1} (consistent forward/adjoint preconditioner)
     double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
     double2* Rinv_rows = dev<double2>(ctx.Rinv_rows, size_t(m) * size_t(m));
-    if (!rinv_ready) {  // (the one-pass Cholesky preconditioner already left R'^{-1} in ctx.Rinv)
-        MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, Rtop, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
-                                   cudaMemcpyDeviceToDevice, ctx.stream));
-        size_t dws = 0, hws = 0;
-        cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
-                                                   CUDA_C_64F, Rinv, m, &dws, &hws),
-                       "trtri_bufferSize");
-        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
-        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
-        cusolver_check(cusolverDnXtrtri(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m, CUDA_C_64F, Rinv,
-                                        m, work, dws, ctx.host_work.data(), hws, dev<int>(ctx.qr_info, 1)),
-                       "trtri");
-    }
+    if (!rinv_ready) upper_inverse(ctx, Rtop, ldR, m, Rinv);  // (else the one-pass Cholesky path left it)
     launch_transpose(Rinv, m, m, m, Rinv_rows, m, ctx.stream);
     ctx.launches += 1;
 
@@ -440,16 +457,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         // >= 1, lsq.cpp:66-69, move by < 1e-3): no Q1, no second pass, and R'^{-1} (which the CG
         // forms anyway) is left in ctx.Rinv.
         double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
-        MNB_CUDA(cudaMemcpyAsync(Rinv, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
-        size_t dws = 0, hws = 0;
-        cusolver_check(cusolverDnXtrtri_bufferSize(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m,
-                                                   CUDA_C_64F, Rinv, m, &dws, &hws),
-                       "trtri_bufferSize");
-        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
-        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
-        cusolver_check(cusolverDnXtrtri(ctx.cusolver, CUBLAS_FILL_MODE_UPPER, CUBLAS_DIAG_NON_UNIT, m, CUDA_C_64F, Rinv,
-                                        m, work, dws, ctx.host_work.data(), hws, info),
-                       "trtri");
+        upper_inverse(ctx, G, m, m, Rinv);
         double nr = 0.0, nri = 0.0;  // lower triangles are zero
         cublas_check(cublasDznrm2(ctx.cublas, int(m * m), reinterpret_cast<const cuDoubleComplex*>(G), 1, &nr), "dznrm2");
         cublas_check(cublasDznrm2(ctx.cublas, int(m * m), reinterpret_cast<const cuDoubleComplex*>(Rinv), 1, &nri),

@@ -540,12 +540,24 @@ __global__ void __launch_bounds__(kUpdWarps * 32) pcg_upd1_kernel(const double* 
     double my = 0.0;
     if (j < m) {
         const double2* col = Rinv + j * m;  // column j of Rinv: entries i <= j
-        double2 acc = make_double2(0.0, 0.0);
-        for (int64_t i = lane; i <= j; i += 32) {
-            const double2 a = col[i], b = s_sh[i];
-            acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));  // conj(a) * b
-            acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+        // four independent accumulators (four loads in flight per lane), combined in fixed order
+        double2 ac[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                         make_double2(0.0, 0.0)};
+        int64_t i = lane;
+        for (; i + 96 <= j; i += 128) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double2 a = col[i + 32 * k], b = s_sh[i + 32 * k];
+                ac[k].x = fma(a.x, b.x, fma(a.y, b.y, ac[k].x));  // conj(a) * b
+                ac[k].y = fma(a.x, b.y, fma(-a.y, b.x, ac[k].y));
+            }
         }
+        for (; i <= j; i += 32) {
+            const double2 a = col[i], b = s_sh[i];
+            ac[0].x = fma(a.x, b.x, fma(a.y, b.y, ac[0].x));
+            ac[0].y = fma(a.x, b.y, fma(-a.y, b.x, ac[0].y));
+        }
+        double2 acc = c_add(c_add(ac[0], ac[1]), c_add(ac[2], ac[3]));
         acc = warp_sum2(acc);
         if (lane == 0) {
             double2 gj;
@@ -633,12 +645,23 @@ __global__ void __launch_bounds__(kUpdWarps * 32) pcg_upd2_kernel(const double* 
     const int64_t i = int64_t(blockIdx.x) * kUpdWarps + warp;
     if (i < m) {
         const double2* row = Rinv_rows + i * m;  // row i of Rinv: entries j >= i
-        double2 acc = make_double2(0.0, 0.0);
-        for (int64_t jj = i + lane; jj < m; jj += 32) {
-            const double2 a = row[jj], b = d_sh[jj];
-            acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-            acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+        double2 ac[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                         make_double2(0.0, 0.0)};
+        int64_t jj = i + lane;
+        for (; jj + 96 < m; jj += 128) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const double2 a = row[jj + 32 * k], b = d_sh[jj + 32 * k];
+                ac[k].x = fma(a.x, b.x, fma(-a.y, b.y, ac[k].x));
+                ac[k].y = fma(a.x, b.y, fma(a.y, b.x, ac[k].y));
+            }
         }
+        for (; jj < m; jj += 32) {
+            const double2 a = row[jj], b = d_sh[jj];
+            ac[0].x = fma(a.x, b.x, fma(-a.y, b.y, ac[0].x));
+            ac[0].y = fma(a.x, b.y, fma(a.y, b.x, ac[0].y));
+        }
+        double2 acc = c_add(c_add(ac[0], ac[1]), c_add(ac[2], ac[3]));
         acc = warp_sum2(acc);
         if (lane == 0) {
             w[i] = acc;

@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--classical", action="store_true",
+                    help="also time the device classical solve (solve_classical, the paper's t0) on the same A")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -343,6 +345,21 @@ def main():
     except Exception:
         pass
     last = reps[-1]
+    classical = None
+    if args.classical and not cfg["real"]:
+        # the paper's comparison t0 / t_r (Tables 1-4) on the GPU: same A (device-resident), same b
+        times = []
+        for _ in range(2):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            xc, crep = mn.solve_classical(inst, ctx, report=True)
+            times.append(time.perf_counter() - t0)
+        xr = last.x.cpu().numpy() if hasattr(last.x, "cpu") else np.asarray(last.x)
+        classical = {"seconds": min(times), "path": crep.path, "refinements": crep.refinements,
+                     "residual_norm": crep.residual_norm,
+                     "rel_diff_randomized": float(np.linalg.norm(xr[:n_local] - xc) / np.linalg.norm(xc)),
+                     "ratio_t0_over_tr": min(times) / value if value else None,
+                     "note": "wall clock of mnb_solve_classical with A in HBM (x to host); value is t_r"}
     sk = last.extra["sketch_kernel_ms"]
     launches = sum(r.extra["kernel_launches"] for r in reps)
 
@@ -399,6 +416,7 @@ def main():
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "pcg_pass_kernel",
                          "peak_kind": peak_kind, "bytes_per_launch": pass_bytes, "ms_per_launch": pass_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            **({"classical": classical} if classical else {}),
             "solve": {"lsq_iterations": last.lsq_iterations, "lsq_converged": last.lsq_converged,
                       "residual_norm": last.residual_norm, "c_norm_ratio": last.c_norm_ratio,
                       "step_seconds": last.step_seconds, "param_seconds": last.extra["param_seconds"],

@@ -124,6 +124,25 @@ void mnb_solver_config_default(mnb_solver_config* cfg);
 int mnb_solve_randomized(mnb_context* ctx, const void* b, int b_location, const mnb_solver_config* cfg,
                          void* x_out, int x_location, void* c_out, mnb_solve_report* report);
 
+/* ---- the classical solver (include/minnorm/solver.hpp:59; src/solver.cpp:130-146) ----
+ * The deterministic O(m^2 n) baseline the paper compares against (t0 of Tables 1-4).
+ * On the GPU: Gram G = A A^H (tensor-core ZHERK; one allreduce across ranks), R1 = chol(G),
+ * and the corrected seminormal equations z_{k+1} = z_k + G^{-1}(b - A A^H z_k), x = A^H z,
+ * each correction one fused pass over A; accepted once ||b - A x|| is at the rounding level
+ * of A x.  When u cond(A)^2 is not small (the Cholesky fails or the corrections do not
+ * contract) it falls back to Householder QR of A^H (cuSOLVER Xgeqrf + Xunmqr; one GPU),
+ * the reference's algorithm without the column pivoting.  Complex A only.
+ * b: m complex values; x_out: this rank's n_local complex values.                        */
+typedef struct {
+    int32_t path;          /* 0 Gram + corrected seminormal equations, 1 Householder QR of A^H */
+    int32_t refinements;   /* corrections taken on path 0                                       */
+    double residual_norm;  /* ||A x - b||                                                        */
+    double seconds;        /* wall time of the call                                              */
+} mnb_classical_report;
+
+int mnb_solve_classical(mnb_context* ctx, const void* b, int b_location, void* x_out, int x_location,
+                        mnb_classical_report* report);
+
 /* ---- the least-squares subsolver (include/minnorm/lsq.hpp:12-40) --------- */
 typedef struct {
     int64_t sketch_size;    /* LsqConfig::sketch_size                                   */

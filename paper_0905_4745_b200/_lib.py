@@ -58,6 +58,11 @@ class LsqConfigC(ctypes.Structure):
                 ("stream_seed", ctypes.c_uint64), ("sampling", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
+class ClassicalReportC(ctypes.Structure):
+    _fields_ = [("path", ctypes.c_int32), ("refinements", ctypes.c_int32), ("residual_norm", ctypes.c_double),
+                ("seconds", ctypes.c_double)]
+
+
 class LsqSolutionC(ctypes.Structure):
     _fields_ = [("achieved_excess", ctypes.c_double), ("iterations", ctypes.c_int64),
                 ("converged", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
@@ -67,7 +72,8 @@ class LsqSolutionC(ctypes.Structure):
 EXPORTS = [
     "mnb_last_error", "mnb_last_deficient_columns", "mnb_version", "mnb_context_create", "mnb_nccl_unique_id",
     "mnb_context_create_distributed", "mnb_context_destroy", "mnb_context_set_stream", "mnb_shard_columns",
-    "mnb_set_matrix", "mnb_solver_config_default", "mnb_solve_randomized", "mnb_solve_least_squares",
+    "mnb_set_matrix", "mnb_solver_config_default", "mnb_solve_randomized", "mnb_solve_classical",
+    "mnb_solve_least_squares",
     "mnb_srft_build", "mnb_srft_from_fields", "mnb_srft_destroy", "mnb_srft_get_field", "mnb_srft_dims",
     "mnb_srft_apply_h", "mnb_srft_apply", "mnb_srft_apply_adjoint", "mnb_srft_apply_to_columns", "mnb_dft",
     "mnb_bench_pcg_pass",
@@ -112,6 +118,7 @@ def load():
                                        ctypes.POINTER(SolveReportC)]
     L.mnb_solve_least_squares.argtypes = [vp, dp, ci, ctypes.POINTER(LsqConfigC), dp, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(LsqSolutionC)]
+    L.mnb_solve_classical.argtypes = [vp, dp, ci, dp, ci, ctypes.POINTER(ClassicalReportC)]
     L.mnb_srft_build.argtypes = [i64, i64, u64, ci, pvp]
     L.mnb_srft_from_fields.argtypes = [i64, i64, ci] + [dp] * 8 + [pvp]
     L.mnb_srft_destroy.argtypes = [vp]

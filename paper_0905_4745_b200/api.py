@@ -330,6 +330,42 @@ class LsqConfig:
 
 
 @dataclass
+class ClassicalReport:
+    """mnb_classical_report (include/minnorm_b200.h): the path taken and its diagnostics."""
+    path: int           # 0 Gram + corrected seminormal equations, 1 Householder QR of A^H
+    refinements: int
+    residual_norm: float
+    seconds: float
+
+
+def solve_classical(inst: ProblemInstance, ctx: Optional[Context] = None, report: bool = False):
+    """solve_classical (include/minnorm/solver.hpp:59; src/solver.cpp:130-146) on the GPU:
+    the minimal-norm x of A x = b by the deterministic O(m^2 n) method (the paper's t0
+    baseline).  Returns x (this rank's entries), or (x, ClassicalReport) with report=True.
+    Raises like the reference: DimensionError, RankDeficiencyError."""
+    ctx = ctx or default_context()
+    A = inst.A
+    if A is not None:
+        if len(inst.b) != A.shape[0]:
+            raise DimensionError(f"right-hand side length {len(inst.b)} does not match m={A.shape[0]}")
+        if ctx.world_size == 1:
+            ctx.set_matrix(A)
+        else:
+            ctx.set_matrix(A, n_global=ctx.n, col_begin=ctx.col_begin)
+    b = _host_c128(inst.b.cpu().numpy() if _is_torch_cuda(inst.b) else inst.b)
+    x = np.zeros(ctx.n_local, np.complex128)
+    rc = L.ClassicalReportC()
+    try:
+        _check(ctx._lib.mnb_solve_classical(ctx._h, _ptr(b), L.MNB_HOST, _ptr(x), L.MNB_HOST, ctypes.byref(rc)))
+    finally:
+        if A is not None and not _is_torch_cuda(A):
+            ctx._keep = None
+    rep = ClassicalReport(path=int(rc.path), refinements=int(rc.refinements), residual_norm=float(rc.residual_norm),
+                          seconds=float(rc.seconds))
+    return (x, rep) if report else x
+
+
+@dataclass
 class LsqSolution:
     """include/minnorm/lsq.hpp:20-26"""
     y: np.ndarray

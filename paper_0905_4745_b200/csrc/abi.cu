@@ -241,6 +241,27 @@ int mnb_solve_randomized(mnb_context* ctx, const void* b, int b_location, const 
     });
 }
 
+int mnb_solve_classical(mnb_context* ctx, const void* b, int b_location, void* x_out, int x_location,
+                        mnb_classical_report* report) {
+    return guard([&] {
+        auto& c = ctx->ctx;
+        MNB_CUDA(cudaSetDevice(c.device));
+        std::vector<double2> bh(size_t(c.m));
+        if (b_location == MNB_DEVICE)
+            MNB_CUDA(cudaMemcpy(bh.data(), b, size_t(c.m) * 16, cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(bh.data(), b, size_t(c.m) * 16);
+        const size_t nb = size_t(std::max<int64_t>(c.n_local, 1)) * 16;
+        double2* x_dev = x_location == MNB_DEVICE ? static_cast<double2*>(x_out)
+                                                  : static_cast<double2*>(c.vec_n[3].ensure(nb));
+        mnb_classical_report rep{};
+        mnb::solve_classical(c, bh.data(), x_dev, rep);
+        if (x_location != MNB_DEVICE && c.n_local) copy_out(x_out, x_dev, size_t(c.n_local) * 16, MNB_HOST, c.stream);
+        mnb::sync(c);
+        if (report) *report = rep;
+    });
+}
+
 int mnb_solve_least_squares(mnb_context* ctx, const void* cvec, int c_location, const mnb_lsq_config* cfg, void* y_out,
                             double* residual_norms, mnb_lsq_solution* sol) {
     return guard([&] {

@@ -186,6 +186,7 @@ void sync(Context& ctx);
 void trace(const char* what);  // MNB_TRACE=1: host phase timestamps on stderr
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep);
+void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_classical_report& rep);
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
                          double* residual_norms, mnb_lsq_solution& sol);
 double bench_pcg_pass(Context& ctx, int reps);

@@ -220,3 +220,18 @@ void launch_cg_init_vectors(const double2* c, int64_t n, double2* r, double2* t,
 }
 
 }  // namespace mnb
+
+namespace mnb {
+namespace {
+__global__ void conj_inplace_kernel(double2* x, int64_t count) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        x[i].y = -x[i].y;
+}
+}  // namespace
+
+void launch_conj_inplace(double2* x, int64_t count, cudaStream_t stream) {
+    if (count <= 0) return;
+    conj_inplace_kernel<<<unsigned(std::min<int64_t>(ceil_div(count, 256), 148 * 16)), 256, 0, stream>>>(x, count);
+    MNB_LAUNCH_CHECK();
+}
+}  // namespace mnb

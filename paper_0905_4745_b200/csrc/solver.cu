@@ -1029,6 +1029,199 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.total_seconds = now_s() - t_start;
 }
 
+// ------------------------------------------------------ solve_classical ----
+// solve_classical (src/solver.cpp:130-146): the deterministic O(m^2 n) baseline.  See
+// include/minnorm_b200.h for the two paths.  Path 0 is the Gram-matrix form of the same
+// minimal-norm solution, x = A^H (A A^H)^{-1} b, made as accurate as the QR form by corrections
+// (each one fused pass: t = A^H z and A t in one read of A); path 1 is the reference's
+// Householder QR of A^H without the column pivoting (a full-rank A needs none for x).
+void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_classical_report& rep) {
+    const double t_start = now_s();
+    validate_matrix_set(ctx);
+    rep = mnb_classical_report{};
+    const int64_t m = ctx.m, n = ctx.n_global;
+    if (m < 1 || m >= n)
+        throw Error(MNB_ERR_DIMENSION, "problem must be underdetermined: 1 <= m < n, got m=" + std::to_string(m) +
+                                           ", n=" + std::to_string(n));
+    if (ctx.dtype != MNB_C128) throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: complex128 A only");
+    bool b_zero = true, b_finite = true;
+    for (int64_t i = 0; i < 2 * m; ++i) {
+        const double v = reinterpret_cast<const double*>(b_host)[i];
+        b_finite = b_finite && std::isfinite(v);
+        b_zero = b_zero && v == 0.0;
+    }
+    if (!b_finite) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
+    ctx.make_resident();
+    const int64_t nl = ctx.n_local;
+    if (b_zero) {  // src/solver.cpp:134
+        if (nl) MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(nl) * 16, ctx.stream));
+        sync(ctx);
+        rep.seconds = now_s() - t_start;
+        return;
+    }
+    const auto* Ac = reinterpret_cast<const cuDoubleComplex*>(ctx.A);
+    double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
+    int* info = dev<int>(ctx.qr_info, 2);
+    // ---- path 0: G = A A^H = R1^H R1
+    bool ok = true;
+    {
+        const double one = 1.0, zero = 0.0;
+        if (nl) cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, int(m), int(nl), &one, Ac,
+                                         int(m), &zero, reinterpret_cast<cuDoubleComplex*>(G), int(m)),
+                             "zherk");
+        else MNB_CUDA(cudaMemsetAsync(G, 0, size_t(m) * size_t(m) * 16, ctx.stream));
+        allreduce_sum(ctx, reinterpret_cast<double*>(G), size_t(2 * m * m));
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXpotrf_bufferSize(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m,
+                                                   CUDA_C_64F, G, m, CUDA_C_64F, &dws, &hws),
+                       "potrf_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXpotrf(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m, CUDA_C_64F, G, m,
+                                        CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
+                       "potrf");
+        int info_h = 0;
+        std::vector<double> diag(size_t(2 * m));
+        MNB_CUDA(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        MNB_CUDA(cudaMemcpy2DAsync(diag.data(), 16, G, size_t(m + 1) * 16, 16, size_t(m), cudaMemcpyDeviceToHost,
+                                   ctx.stream));
+        sync(ctx);
+        double dmax = 0.0, dmin = 1e300;
+        for (int64_t j = 0; j < m; ++j) {
+            const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
+            dmax = std::max(dmax, a);
+            dmin = std::min(dmin, a);
+        }
+        ok = info_h == 0 && dmin > 0.0 && dmax / dmin < 1e7;
+    }
+    if (ok) {
+        launch_zero_lower(G, m, ctx.stream);  // potrf leaves the strict lower triangle unreferenced
+        ctx.launches += 1;
+        double fro = 0.0;  // ||R1||_F = sqrt(trace G) = ||A||_F
+        cublas_check(cublasDznrm2(ctx.cublas, int(m * m), reinterpret_cast<const cuDoubleComplex*>(G), 1, &fro),
+                     "dznrm2");
+        const double thr = 2.0 * std::sqrt(double(n)) * kEps * fro;  // rounding level of ||A x|| / ||x||
+        PassBuffers pb = pass_buffers(ctx);
+        double2* zd = dev<double2>(ctx.vec_m[0], size_t(m));
+        double2* dx = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(nl, 1)));
+        double* scal = dev<double>(ctx.scratch, 1024);
+        std::vector<double2> r(b_host, b_host + m), s(static_cast<size_t>(m)), ax(static_cast<size_t>(m));
+        double prev = 0.0;
+        ok = false;
+        // x is kept explicitly and corrected, x_{k+1} = x_k + A^H G^{-1} (b - A x_k) (Bjorck's corrected
+        // seminormal equations): each step one fused pass gives dx = A^H dz and A dx together.
+        for (int it = 0; it <= 4; ++it) {
+            MNB_CUDA(cudaMemcpyAsync(zd, r.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+            cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
+                                     reinterpret_cast<const cuDoubleComplex*>(G), int(m),
+                                     reinterpret_cast<cuDoubleComplex*>(zd), 1),
+                         "ztrsv");
+            cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
+                                     reinterpret_cast<const cuDoubleComplex*>(G), int(m),
+                                     reinterpret_cast<cuDoubleComplex*>(zd), 1),
+                         "ztrsv");
+            fused_pass(ctx, pb, PCG_APPLY, zd, nullptr, it == 0 ? x_dev : dx, nullptr, nullptr);
+            MNB_CUDA(cudaMemcpyAsync(s.data(), pb.red, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
+            if (it > 0 && nl) {
+                const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+                cublas_check(cublasZaxpy(ctx.cublas, int(nl), &one, reinterpret_cast<const cuDoubleComplex*>(dx), 1,
+                                         reinterpret_cast<cuDoubleComplex*>(x_dev), 1),
+                             "zaxpy");
+            }
+            double xn = 0.0;  // ||x||: this rank's part, summed over ranks
+            if (nl) cublas_check(cublasDznrm2(ctx.cublas, int(nl), reinterpret_cast<const cuDoubleComplex*>(x_dev), 1, &xn),
+                                 "dznrm2");
+            xn *= xn;
+            MNB_CUDA(cudaMemcpyAsync(scal, &xn, sizeof(double), cudaMemcpyHostToDevice, ctx.stream));
+            allreduce_sum(ctx, scal, 1);
+            MNB_CUDA(cudaMemcpyAsync(&xn, scal, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+            sync(ctx);
+            double rn = 0.0;
+            for (int64_t i = 0; i < m; ++i) {
+                ax[size_t(i)] = it == 0 ? s[size_t(i)]
+                                        : make_double2(ax[size_t(i)].x + s[size_t(i)].x, ax[size_t(i)].y + s[size_t(i)].y);
+                r[size_t(i)] = make_double2(b_host[i].x - ax[size_t(i)].x, b_host[i].y - ax[size_t(i)].y);
+                rn += r[size_t(i)].x * r[size_t(i)].x + r[size_t(i)].y * r[size_t(i)].y;
+            }
+            rn = std::sqrt(rn);
+            rep.refinements = it;
+            rep.residual_norm = rn;
+            // keep correcting while the residual still halves (the forward error follows it down,
+            // times cond(A)); accept once it stagnates at the rounding level of A x
+            const bool at_floor = rn <= thr * std::sqrt(xn);
+            if (it > 0 && !(rn < 0.5 * prev)) {
+                ok = at_floor;  // stagnated: at the floor (done) or above it (u cond(A)^2 too large)
+                break;
+            }
+            if (it == 4) {
+                ok = at_floor;
+                break;
+            }
+            prev = rn;
+        }
+        rep.path = 0;
+    }
+    if (!ok) {
+        // ---- path 1: Householder QR of A^H (n x m), x = Q [R^{-H} b; 0]
+        if (ctx.world > 1)
+            throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: A is too ill-conditioned for the Gram path and the "
+                                             "Householder fallback runs on one GPU");
+        double2* AH = dev<double2>(ctx.ws_x1, size_t(n) * size_t(m));
+        launch_transpose(static_cast<const double2*>(ctx.A), m, n, m, AH, n, ctx.stream);
+        launch_conj_inplace(AH, n * m, ctx.stream);
+        ctx.launches += 2;
+        double2* tau = dev<double2>(ctx.tau_S, size_t(m));
+        size_t dws = 0, hws = 0;
+        cusolver_check(cusolverDnXgeqrf_bufferSize(ctx.cusolver, ctx.cusolver_params, n, m, CUDA_C_64F, AH, n,
+                                                   CUDA_C_64F, tau, CUDA_C_64F, &dws, &hws),
+                       "geqrf_bufferSize");
+        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+        cusolver_check(cusolverDnXgeqrf(ctx.cusolver, ctx.cusolver_params, n, m, CUDA_C_64F, AH, n, CUDA_C_64F, tau,
+                                        CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
+                       "geqrf");
+        // the reference's rank rule with threshold n eps max|R_jj| (src/solver.cpp:137-140)
+        if (int64_t bad = deficient_count(ctx, AH, n, m, n); bad > 0)
+            throw Error(MNB_ERR_RANK_DEFICIENCY,
+                        "pivoted QR found rank deficiency (" + std::to_string(bad) + " dependent columns)", bad);
+        MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(n) * 16, ctx.stream));
+        MNB_CUDA(cudaMemcpyAsync(x_dev, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
+                                 reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
+                                 reinterpret_cast<cuDoubleComplex*>(x_dev), 1),
+                     "ztrsv");
+        int lwork = 0;
+        cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(n), 1, int(m),
+                                                   reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
+                                                   reinterpret_cast<const cuDoubleComplex*>(tau),
+                                                   reinterpret_cast<const cuDoubleComplex*>(x_dev), int(n), &lwork),
+                       "unmqr_bufferSize");
+        auto* wk = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
+        cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(n), 1, int(m),
+                                        reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
+                                        reinterpret_cast<const cuDoubleComplex*>(tau),
+                                        reinterpret_cast<cuDoubleComplex*>(x_dev), int(n), wk, lwork, info),
+                       "unmqr");
+        // ||A x - b|| through the INIT pass (s = A x)
+        PassBuffers pb = pass_buffers(ctx);
+        double2* r1 = dev<double2>(ctx.vec_n[0], size_t(n));
+        double2* t1 = dev<double2>(ctx.vec_n[1], size_t(n));
+        fused_pass(ctx, pb, PCG_INIT, nullptr, x_dev, t1, r1, nullptr, nullptr);
+        std::vector<double2> s(static_cast<size_t>(m));
+        MNB_CUDA(cudaMemcpyAsync(s.data(), pb.red, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
+        sync(ctx);
+        double rn = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+            const double dr = b_host[i].x - s[size_t(i)].x, di = b_host[i].y - s[size_t(i)].y;
+            rn += dr * dr + di * di;
+        }
+        rep.path = 1;
+        rep.residual_norm = std::sqrt(rn);
+    }
+    sync(ctx);
+    rep.seconds = now_s() - t_start;
+}
+
 // ------------------------------------------------ solve_least_squares -----
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
                          double* residual_norms, mnb_lsq_solution& sol) {

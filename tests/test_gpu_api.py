@@ -227,3 +227,44 @@ def test_pinned_host_matrix_pipelined_copy_matches(ctx):
     S1 = op.sketch(ctx)
     ctx.set_matrix(np.asfortranarray(A))
     assert np.array_equal(S1, op.sketch(ctx))
+
+
+# ---- solve_classical (src/solver.cpp:130-146) on the GPU ----------------------------------
+@pytest.mark.parametrize("m,n,kappa,path", [(64, 1024, 1e3, 0), (256, 16384, 1e6, 0), (128, 8192, 1e8, 1),
+                                            (16, 6000, 1e2, 0)])
+def test_solve_classical_matches_oracle(ctx, m, n, kappa, path):
+    """The device classical solver (Gram + corrected seminormal equations, or Householder QR
+    of A^H when u cond(A)^2 is not small) against the oracle's pivoted-QR solve_classical:
+    the same minimal-norm x to within the problem's conditioning (1e-13 kappa), a residual at
+    the rounding level, and the path the header documents."""
+    A, b = make_instance(m, n, kappa, seed=m + 21)
+    x, rep = mn.solve_classical(mn.ProblemInstance(A, b), ctx, report=True)
+    p = O.solve_classical(A, b)
+    assert np.linalg.norm(x - p) / np.linalg.norm(p) <= max(1e-14 * kappa, 1e-12)
+    assert rep.path == path
+    assert abs(rep.residual_norm - np.linalg.norm(A @ x - b)) <= 1e-6 * np.linalg.norm(b) + 1e-3 * rep.residual_norm
+    assert rep.residual_norm <= 1e-12 * np.linalg.norm(A, 2) * np.linalg.norm(x) * np.sqrt(n)
+
+
+def test_solve_classical_zero_rhs_and_errors(ctx):
+    """b = 0 gives x = 0 (src/solver.cpp:134); a rank-deficient A raises RankDeficiencyError;
+    a wrong-length b raises DimensionError (ProblemInstance::validate)."""
+    A, b = make_instance(32, 512, 1e2, seed=4)
+    x = mn.solve_classical(mn.ProblemInstance(A, np.zeros(32, np.complex128)), ctx)
+    assert np.all(x == 0)
+    Ad = A.copy()
+    Ad[5] = Ad[3]  # two equal rows: rank m - 1
+    with pytest.raises(mn.RankDeficiencyError):
+        mn.solve_classical(mn.ProblemInstance(Ad, b), ctx)
+    with pytest.raises(mn.DimensionError):
+        mn.solve_classical(mn.ProblemInstance(A, b[:5]), ctx)
+
+
+def test_solve_classical_agrees_with_randomized(ctx):
+    """The paper's comparison (Tables 1-4): the randomized solve matches the classical one to
+    its epsilon."""
+    A, b = make_instance(128, 4096, 1e4, seed=9)
+    cfg = mn.SolverConfig(epsilon=1e-10, seed=42)
+    xr = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx).x
+    xc = mn.solve_classical(mn.ProblemInstance(A, b), ctx)
+    assert np.linalg.norm(xr - xc) / np.linalg.norm(xc) <= 10 * cfg.epsilon

@@ -2,24 +2,27 @@
 // n = n1 x 1024 (n1 = 1024 or 3072) with rotation-chain chunks of n1 indices.
 //
 // The unfused path runs P2 (x2 = D Chain(x1[:, p_i]), src/srft.cpp:56-57,128)
-// and then pass A (length-1024 DFTs over k2 of x2[:, k1 + 1024 k2]) as two
+// and then pass A (length-1024 DFTs over k2 of x2[:, k1 + n1 k2]) as two
 // launches with x2 (16 B per element) written to HBM and read back.  But
 // chunk c of P2's chain IS k2 = c, and every chunk walks its k1 range in the
 // same (descending) order: if all 1024 chunks of a row block advance in
-// lock step, step s produces x2[:, k1 + 1024 k2] for one k1 = 1023 - s and
-// every k2 -- exactly one pass-A transform.  So one CTA owns 4 rows and all
-// 1024 chunks (a cluster pair covers an 8-row block); each step it
-//   1. advances 16 chains per thread (row r, chunks c = u + 64 q) with the
-//      gathered x1 values it prefetched during the previous step (a 64-byte
+// lock step, step s produces x2[:, k1 + n1 k2] for one k1 = n1 - 1 - s and
+// every k2 -- exactly one pass-A transform.  So one CTA (512 threads) owns 4
+// rows and all 1024 chunks (a cluster pair covers an 8-row block); each step it
+//   1. advances 8 chains per thread (row r, chunks c = u + 128 q) with the
+//      gathered x1 values that landed during the previous step (a 64-byte
 //      piece of 4 rows per gathered index, the 4 row-lanes of a chunk coalesced;
 //      the cluster partner reads the other half of the 128-byte piece),
-//   2. transforms the 1024 chain outputs of each row in registers + shared
-//      memory (radix 16 x 16 x 4; the chain outputs already sit in the
-//      radix-16 input order, c = u + 64 q),
+//   2. transforms the 1024 chain outputs of each row: radix 8 in registers (the
+//      chain outputs already sit in its input order), radix 8 and radix 16 through
+//      two shared-memory exchanges, the last radix 2 of the radix 16 by shuffles,
 //   3. applies the four-step twiddle w_n^{f2 k1} and stores the 1024 results
 //      per row in the blocked layout [row block][f2][k1][8] pass B reads.
 // x2 never exists in HBM: the sketch reads x1 once and writes pass A's output
-// once (2 x 16 B per element instead of 4 x 16 B).
+// once (2 x 16 B per element instead of 4 x 16 B).  A row block whose 1024 (or
+// n1) steps would leave most pairs idle in the last round runs as two k1
+// segments, the second restarted like a chunk boundary (restart table of n1/2-
+// index sub-chunks).
 //
 // Chain arithmetic (rotation_chain_scalar, src/kernels_scalar.cpp:15-24) is
 // the hchain_kernel's, operation for operation (same _rn intrinsics, same
@@ -55,7 +58,7 @@ constexpr int kPad = 17;       // stage-3 exchange rows padded to 17 entries (ba
 // PRM, IDX and Z come from step-major tables (build_p2fa_tables) with one TMA bulk
 // copy each per step, issued by thread 0 a phase ahead of their use.  The two CTAs
 // of a cluster own rows 0-3 and 4-7 of one 8-row block and advance in lock step (a
-// cluster barrier every few steps), so their 64-byte halves of every gathered
+// cluster barrier every 16 steps), so their 64-byte halves of every gathered
 // 128-byte piece reach L2 together (the loads ask L2 for the whole line) and the
 // blocked stores of the pair fill whole lines.
 struct P2faSmem {

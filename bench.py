@@ -338,10 +338,12 @@ def main():
     pass_bytes = esz * m * n_local + 64 * n_local  # A once + the lagged r / t n-vectors (read + write)
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     traffic = None
+    traffic_sketch = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f).get(args.config, {})
         traffic = prof.get("pcg_pass_dram_bytes_per_launch")
+        traffic_sketch = prof.get("p2fa_dram_bytes_per_launch")
     except Exception:
         pass
     last = reps[-1]
@@ -404,6 +406,18 @@ def main():
         sketch_ms = {"hstage1": sk[0], "hstage2+fft_a": sk[1], "fft_b": sk[3]}
         sketch_gbs = {"hstage1": gbs(esz + 16, sk[0]), "hstage2+fft_a": gbs(32, sk[1]), "fft_b": gbs(16, sk[3])}
 
+    # the sketch's dominant kernel against the same HBM peak: the fused H stage + FFT pass A moves
+    # 16 B in (x1) and 16 B out (pass A's output) per element; kernel time summed over both sketches
+    roofline_sketch = None
+    if sk[2] == 0 and sk[1] > 0:
+        per_sketch_bytes = 32 * m * n
+        ach = 2 * per_sketch_bytes / (sk[1] * 1e-3) / 1e9
+        roofline_sketch = {"bound": "hbm", "kernel": "p2fa_kernel", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                           "frac": ach / hbm_peak, "bytes_per_sketch": per_sketch_bytes,
+                           "ms_per_sketch": sk[1] / 2,
+                           "traffic": traffic_sketch if world == 1 else None,
+                           "note": "one launch per sketch at c4 (one per row slab at c5); traffic per launch at c4"}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -415,6 +429,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "kernel": "pcg_pass_kernel",
                          "peak_kind": peak_kind, "bytes_per_launch": pass_bytes, "ms_per_launch": pass_ms},
+            **({"roofline_sketch": roofline_sketch} if roofline_sketch else {}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             **({"classical": classical} if classical else {}),
             "solve": {"lsq_iterations": last.lsq_iterations, "lsq_converged": last.lsq_converged,

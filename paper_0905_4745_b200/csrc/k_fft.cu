@@ -544,29 +544,18 @@ __global__ void __launch_bounds__(512, 1) fft1024_select_kernel(const FftPassArg
         dft16_np<false>(v);
         for (int b0 = 0; b0 < cnt; b0 += kSB) {
             const int nb = min(kSB, cnt - b0);
-            // two samples per iteration (independent chains); Y_u[f mod 16] picked from the
-            // registers by predicated selects (a runtime index would spill v to local memory)
-            auto pick = [&](int j) {
-                double2 y = v[0];
 #pragma unroll
-                for (int q = 1; q < 16; ++q) y = (j == q) ? v[d16(q)] : y;
-                return y;
-            };
-            for (int s = b0; s < b0 + nb; s += 2) {  // warp-uniform bounds: the shuffles are convergent
-                const bool two = s + 1 < b0 + nb;
-                const int f0 = E[2 * s], f1 = two ? E[2 * (s + 1)] : f0;
-                double2 p0 = c_mul(pick(f0 & 15), W[(f0 * u) & (N - 1)]);
-                double2 p1 = c_mul(pick(f1 & 15), W[(f1 * u) & (N - 1)]);
+            for (int j = 0; j < 16; ++j) {
+                const int lo = max(JOFF[j], b0), hi = min(JOFF[j + 1], b0 + nb);
+                for (int s = lo; s < hi; ++s) {  // warp-uniform bounds: the shuffles are convergent
+                    const int f = E[2 * s];
+                    double2 p = c_mul(v[d16(j)], W[(f * u) & (N - 1)]);
 #pragma unroll
-                for (int o = 8; o < 32; o <<= 1) {
-                    p0.x += __shfl_xor_sync(0xffffffffu, p0.x, o);
-                    p0.y += __shfl_xor_sync(0xffffffffu, p0.y, o);
-                    p1.x += __shfl_xor_sync(0xffffffffu, p1.x, o);
-                    p1.y += __shfl_xor_sync(0xffffffffu, p1.y, o);
-                }
-                if (lane < 8) {
-                    P[(warp * kSB + (s - b0)) * 8 + lane] = p0;
-                    if (two) P[(warp * kSB + (s + 1 - b0)) * 8 + lane] = p1;
+                    for (int o = 8; o < 32; o <<= 1) {
+                        p.x += __shfl_xor_sync(0xffffffffu, p.x, o);
+                        p.y += __shfl_xor_sync(0xffffffffu, p.y, o);
+                    }
+                    if (lane < 8) P[(warp * kSB + (s - b0)) * 8 + lane] = p;
                 }
             }
             __syncthreads();

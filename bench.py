@@ -348,7 +348,7 @@ def main():
         pass
     last = reps[-1]
     classical = None
-    if args.classical and not cfg["real"]:
+    if args.classical:
         # the paper's comparison t0 / t_r (Tables 1-4) on the GPU: same A (device-resident), same b
         times = []
         for _ in range(2):

@@ -131,7 +131,7 @@ int mnb_solve_randomized(mnb_context* ctx, const void* b, int b_location, const 
  * each correction one fused pass over A; accepted once ||b - A x|| is at the rounding level
  * of A x.  When u cond(A)^2 is not small (the Cholesky fails or the corrections do not
  * contract) it falls back to Householder QR of A^H (cuSOLVER Xgeqrf + Xunmqr; one GPU),
- * the reference's algorithm without the column pivoting.  Complex A only.
+ * the reference's algorithm without the column pivoting (complex A; real A takes path 0 only).
  * b: m complex values; x_out: this rank's n_local complex values.                        */
 typedef struct {
     int32_t path;          /* 0 Gram + corrected seminormal equations, 1 Householder QR of A^H */

@@ -235,3 +235,19 @@ void launch_conj_inplace(double2* x, int64_t count, cudaStream_t stream) {
     MNB_LAUNCH_CHECK();
 }
 }  // namespace mnb
+
+namespace mnb {
+namespace {
+__global__ void real_to_complex_kernel(const double* in, double2* out, int64_t count) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = make_double2(in[i], 0.0);
+}
+}  // namespace
+
+void launch_real_to_complex(const double* in, double2* out, int64_t count, cudaStream_t stream) {
+    if (count <= 0) return;
+    real_to_complex_kernel<<<unsigned(std::min<int64_t>(ceil_div(count, 256), 148 * 16)), 256, 0, stream>>>(in, out,
+                                                                                                            count);
+    MNB_LAUNCH_CHECK();
+}
+}  // namespace mnb

@@ -135,6 +135,8 @@ void launch_zero_lower(double2* A, int64_t m, cudaStream_t stream);
 // library work on another stream)
 void launch_sketch_adjoint_gemv(const double2* S, int64_t l, int64_t m, const double2* z, double2* y,
                                 cudaStream_t stream);
+// out = in + 0i
+void launch_real_to_complex(const double* in, double2* out, int64_t count, cudaStream_t stream);
 // x <- conj(x)
 void launch_conj_inplace(double2* x, int64_t count, cudaStream_t stream);
 // r = c, t = 0, x = 0 (x may be null), red_scal[0..3] = [||c||^2, 0, 0, 0]; part: `parts` doubles of scratch

@@ -1043,7 +1043,6 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
     if (m < 1 || m >= n)
         throw Error(MNB_ERR_DIMENSION, "problem must be underdetermined: 1 <= m < n, got m=" + std::to_string(m) +
                                            ", n=" + std::to_string(n));
-    if (ctx.dtype != MNB_C128) throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: complex128 A only");
     bool b_zero = true, b_finite = true;
     for (int64_t i = 0; i < 2 * m; ++i) {
         const double v = reinterpret_cast<const double*>(b_host)[i];
@@ -1066,10 +1065,20 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
     bool ok = true;
     {
         const double one = 1.0, zero = 0.0;
-        if (nl) cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, int(m), int(nl), &one, Ac,
-                                         int(m), &zero, reinterpret_cast<cuDoubleComplex*>(G), int(m)),
-                             "zherk");
-        else MNB_CUDA(cudaMemsetAsync(G, 0, size_t(m) * size_t(m) * 16, ctx.stream));
+        if (nl && ctx.dtype == MNB_F64) {  // real A: G = A A^T by DSYRK, widened to the complex G
+            double* Gr = dev<double>(ctx.qwork, size_t(m) * size_t(m));
+            cublas_check(cublasDsyrk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, int(m), int(nl), &one,
+                                     static_cast<const double*>(ctx.A), int(m), &zero, Gr, int(m)),
+                         "dsyrk");
+            launch_real_to_complex(Gr, G, m * m, ctx.stream);
+            ctx.launches += 1;
+        } else if (nl) {
+            cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, int(m), int(nl), &one, Ac, int(m),
+                                     &zero, reinterpret_cast<cuDoubleComplex*>(G), int(m)),
+                         "zherk");
+        } else {
+            MNB_CUDA(cudaMemsetAsync(G, 0, size_t(m) * size_t(m) * 16, ctx.stream));
+        }
         allreduce_sum(ctx, reinterpret_cast<double*>(G), size_t(2 * m * m));
         size_t dws = 0, hws = 0;
         cusolver_check(cusolverDnXpotrf_bufferSize(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m,
@@ -1110,7 +1119,7 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
         ok = false;
         // x is kept explicitly and corrected, x_{k+1} = x_k + A^H G^{-1} (b - A x_k) (Bjorck's corrected
         // seminormal equations): each step one fused pass gives dx = A^H dz and A dx together.
-        for (int it = 0; it <= 4; ++it) {
+        for (int it = 0; it <= 8; ++it) {
             MNB_CUDA(cudaMemcpyAsync(zd, r.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
             cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
                                      reinterpret_cast<const cuDoubleComplex*>(G), int(m),
@@ -1153,7 +1162,7 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
                 ok = at_floor;  // stagnated: at the floor (done) or above it (u cond(A)^2 too large)
                 break;
             }
-            if (it == 4) {
+            if (it == 8) {
                 ok = at_floor;
                 break;
             }
@@ -1163,9 +1172,9 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
     }
     if (!ok) {
         // ---- path 1: Householder QR of A^H (n x m), x = Q [R^{-H} b; 0]
-        if (ctx.world > 1)
+        if (ctx.world > 1 || ctx.dtype != MNB_C128)
             throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: A is too ill-conditioned for the Gram path and the "
-                                             "Householder fallback runs on one GPU");
+                                             "Householder fallback runs on one GPU with complex A");
         double2* AH = dev<double2>(ctx.ws_x1, size_t(n) * size_t(m));
         launch_transpose(static_cast<const double2*>(ctx.A), m, n, m, AH, n, ctx.stream);
         launch_conj_inplace(AH, n * m, ctx.stream);

@@ -246,6 +246,15 @@ def test_solve_classical_matches_oracle(ctx, m, n, kappa, path):
     assert rep.residual_norm <= 1e-12 * np.linalg.norm(A, 2) * np.linalg.norm(x) * np.sqrt(n)
 
 
+def test_solve_classical_real_matrix(ctx):
+    """Real A (the c5 type): the Gram path with DSYRK, same x as the oracle."""
+    A, b = make_instance(48, 4096, 1e3, seed=8, real=True)
+    x, rep = mn.solve_classical(mn.ProblemInstance(A, b), ctx, report=True)
+    p = O.solve_classical(A.astype(np.complex128), b)
+    assert rep.path == 0
+    assert np.linalg.norm(x - p) / np.linalg.norm(p) <= 1e-11
+
+
 def test_solve_classical_zero_rhs_and_errors(ctx):
     """b = 0 gives x = 0 (src/solver.cpp:134); a rank-deficient A raises RankDeficiencyError;
     a wrong-length b raises DimensionError (ProblemInstance::validate)."""

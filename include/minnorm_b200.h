@@ -213,6 +213,13 @@ int mnb_dft(mnb_context* ctx, int64_t n, void* x, int inverse);
 /* ---- benchmarking hooks (device-resident, CUDA-event timed) -------------- */
 /* Times `reps` launches of the fused PCG pass s = A(A^H w), qq = ||A^H w||^2
  * over the context matrix; returns the mean per-launch milliseconds. */
+/* Step 5 of solve_randomized as a standalone product (src/solver.cpp:118-125): x = A^H y for
+ * this rank's columns, and (ax_out != NULL) A x = A A^H y summed over ranks -- one fused pass
+ * over A (the PCG pass kernel in its apply mode).  y: m complex (host or device);
+ * x_out: n_local complex; ax_out: m complex (host).                                          */
+int mnb_apply_adjoint_matrix(mnb_context* ctx, const void* y, int y_location, void* x_out, int x_location,
+                             void* ax_out);
+
 int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch);
 
 #ifdef __cplusplus

@@ -6,13 +6,13 @@ The package is a thin Python mirror of the reference's interface
 fused preconditioned-CG pass and the adjoint transform, cuSOLVER for the
 small QR, NCCL for column-sharded multi-GPU runs.
 """
-from .api import (ConfigError, Context, DeviceError, DimensionError, LsqConfig, LsqSolution, ProblemInstance,
+from .api import (apply_adjoint_matrix, ConfigError, Context, DeviceError, DimensionError, LsqConfig, LsqSolution, ProblemInstance,
                   RankDeficiencyError, Sampling, SolveReport, SolverConfig, SrftOperator, UnsupportedError,
                   build_srft, default_context, derive_seed, dft, idft, shard_columns, solve_classical,
                   solve_least_squares, solve_randomized, srft_from_fields, ClassicalReport)
 
 __all__ = [
-    "ConfigError", "Context", "DeviceError", "DimensionError", "LsqConfig", "LsqSolution", "ProblemInstance",
+    "apply_adjoint_matrix", "ConfigError", "Context", "DeviceError", "DimensionError", "LsqConfig", "LsqSolution", "ProblemInstance",
     "RankDeficiencyError", "Sampling", "SolveReport", "SolverConfig", "SrftOperator", "UnsupportedError",
     "build_srft", "default_context", "derive_seed", "dft", "idft", "shard_columns", "solve_classical",
     "solve_least_squares", "solve_randomized", "srft_from_fields", "ClassicalReport",

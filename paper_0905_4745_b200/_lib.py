@@ -76,7 +76,7 @@ EXPORTS = [
     "mnb_solve_least_squares",
     "mnb_srft_build", "mnb_srft_from_fields", "mnb_srft_destroy", "mnb_srft_get_field", "mnb_srft_dims",
     "mnb_srft_apply_h", "mnb_srft_apply", "mnb_srft_apply_adjoint", "mnb_srft_apply_to_columns", "mnb_dft",
-    "mnb_bench_pcg_pass",
+    "mnb_apply_adjoint_matrix", "mnb_bench_pcg_pass",
 ]
 
 _lib = None
@@ -119,6 +119,7 @@ def load():
     L.mnb_solve_least_squares.argtypes = [vp, dp, ci, ctypes.POINTER(LsqConfigC), dp, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(LsqSolutionC)]
     L.mnb_solve_classical.argtypes = [vp, dp, ci, dp, ci, ctypes.POINTER(ClassicalReportC)]
+    L.mnb_apply_adjoint_matrix.argtypes = [vp, dp, ci, dp, ci, dp]
     L.mnb_srft_build.argtypes = [i64, i64, u64, ci, pvp]
     L.mnb_srft_from_fields.argtypes = [i64, i64, ci] + [dp] * 8 + [pvp]
     L.mnb_srft_destroy.argtypes = [vp]

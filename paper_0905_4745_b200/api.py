@@ -329,6 +329,20 @@ class LsqConfig:
     sampling: Sampling = Sampling.without_replacement
 
 
+def apply_adjoint_matrix(y, ctx: Optional[Context] = None, with_ax: bool = False):
+    """x = A^H y for the context matrix (this rank's columns) -- Step 5 of solve_randomized
+    (src/solver.cpp:118-125) -- and, with with_ax, A x (summed over ranks) from the same pass."""
+    ctx = ctx or default_context()
+    y = _host_c128(y)
+    if y.size != ctx.m:
+        raise DimensionError(f"y length {y.size} does not match m={ctx.m}")
+    x = np.zeros(ctx.n_local, np.complex128)
+    ax = np.zeros(ctx.m, np.complex128) if with_ax else None
+    _check(ctx._lib.mnb_apply_adjoint_matrix(ctx._h, _ptr(y), L.MNB_HOST, _ptr(x), L.MNB_HOST,
+                                             _ptr(ax) if ax is not None else None))
+    return (x, ax) if with_ax else x
+
+
 @dataclass
 class ClassicalReport:
     """mnb_classical_report (include/minnorm_b200.h): the path taken and its diagnostics."""

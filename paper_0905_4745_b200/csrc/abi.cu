@@ -431,6 +431,21 @@ int mnb_dft(mnb_context* ctx, int64_t n, void* x, int inverse) {
     });
 }
 
+int mnb_apply_adjoint_matrix(mnb_context* ctx, const void* y, int y_location, void* x_out, int x_location,
+                             void* ax_out) {
+    return guard([&] {
+        auto& c = ctx->ctx;
+        MNB_CUDA(cudaSetDevice(c.device));
+        c.make_resident();
+        const size_t nb = size_t(std::max<int64_t>(c.n_local, 1)) * 16;
+        double2* x_dev = x_location == MNB_DEVICE ? static_cast<double2*>(x_out)
+                                                  : static_cast<double2*>(c.vec_n[3].ensure(nb));
+        mnb::apply_adjoint_matrix(c, y, y_location == MNB_DEVICE, x_dev, static_cast<double2*>(ax_out));
+        if (x_location != MNB_DEVICE && c.n_local) copy_out(x_out, x_dev, size_t(c.n_local) * 16, MNB_HOST, c.stream);
+        mnb::sync(c);
+    });
+}
+
 int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch) {
     return guard([&] {
         MNB_CUDA(cudaSetDevice(ctx->ctx.device));

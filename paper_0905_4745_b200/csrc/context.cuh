@@ -187,6 +187,7 @@ void trace(const char* what);  // MNB_TRACE=1: host phase timestamps on stderr
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep);
 void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_classical_report& rep);
+void apply_adjoint_matrix(Context& ctx, const void* y, bool y_on_device, double2* x_dev, double2* ax_host);
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
                          double* residual_norms, mnb_lsq_solution& sol);
 double bench_pcg_pass(Context& ctx, int reps);

@@ -1029,6 +1029,22 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     rep.total_seconds = now_s() - t_start;
 }
 
+// ------------------------------------------------- apply_adjoint_matrix ----
+// x = A^H y (this rank's columns) and A x (over all ranks) in one fused pass: Step 5 of the
+// solve (src/solver.cpp:118-125) as a standalone product.
+void apply_adjoint_matrix(Context& ctx, const void* y, bool y_on_device, double2* x_dev, double2* ax_host) {
+    validate_matrix_set(ctx);
+    const int64_t m = ctx.m, nl = ctx.n_local;
+    double2* yd = dev<double2>(ctx.vec_m[0], size_t(m));
+    MNB_CUDA(cudaMemcpyAsync(yd, y, size_t(m) * 16, y_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             ctx.stream));
+    PassBuffers pb = pass_buffers(ctx);
+    double2* t = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(nl, 1)));
+    fused_pass(ctx, pb, PCG_APPLY, yd, nullptr, nl ? x_dev : t, nullptr, nullptr);
+    if (ax_host) MNB_CUDA(cudaMemcpyAsync(ax_host, pb.red, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));
+    sync(ctx);
+}
+
 // ------------------------------------------------------ solve_classical ----
 // solve_classical (src/solver.cpp:130-146): the deterministic O(m^2 n) baseline.  See
 // include/minnorm_b200.h for the two paths.  Path 0 is the Gram-matrix form of the same

@@ -277,3 +277,19 @@ def test_solve_classical_agrees_with_randomized(ctx):
     xr = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, ctx).x
     xc = mn.solve_classical(mn.ProblemInstance(A, b), ctx)
     assert np.linalg.norm(xr - xc) / np.linalg.norm(xc) <= 10 * cfg.epsilon
+
+
+def test_apply_adjoint_matrix(ctx):
+    """mnb_apply_adjoint_matrix: x = A^H y and A x from one fused pass (Step 5 of the solve,
+    src/solver.cpp:118-125) against numpy; complex and real A."""
+    for real in (False, True):
+        A, _ = make_instance(40, 3000, 1e2, seed=31, real=real)
+        rng = np.random.default_rng(3)
+        y = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+        ctx.set_matrix(A)
+        x, ax = mn.apply_adjoint_matrix(y, ctx, with_ax=True)
+        xr = A.conj().T @ y
+        assert np.linalg.norm(x - xr) <= 1e-13 * np.linalg.norm(xr)
+        assert np.linalg.norm(ax - A @ xr) <= 1e-13 * np.linalg.norm(A @ xr)
+        with pytest.raises(mn.DimensionError):
+            mn.apply_adjoint_matrix(y[:5], ctx)

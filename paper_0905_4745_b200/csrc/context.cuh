@@ -120,7 +120,7 @@ struct Context {
     int64_t launches = 0;  // own kernels launched (for reporting)
 
     // workspaces
-    DevBuf ws_x1, ws_x2, ws_slab, ws_pack;
+    DevBuf ws_x1, ws_x2, ws_slab, ws_pack, ws_carry;
     DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)

@@ -178,32 +178,14 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
         const int s0 = seg * S, s1 = s0 + S;
         const double2* src = a.x1 + (rb * 8 + kRows * rank + r);
         double2 carry[kQ];
-        // ---- prologue: every chunk's chain from its restart point down to the segment's first
-        //      output (hchain_kernel: carry = x_start; non-storing steps j = start-1 .. B-1, B the
-        //      segment's upper bound; a later segment restarts from the fine restart table)
+        // ---- each chunk's carry at the segment's upper bound, from the restart pass
+        //      (p2fa_carry_kernel: hchain_kernel's non-storing steps, start-1 .. B-1)
         {
-            int32_t j0[kQ];
-            int hmax = 0;
+            const int64_t crow = rb * 8 + kRows * rank + r;
 #pragma unroll
             for (int q = 0; q < kQ; ++q) {
                 const int c = u + 128 * q;
-                const int32_t start = seg == 0 ? __ldg(a.halo + c) : __ldg(a.halo_seg + c * nseg + (nseg - 1 - seg));
-                j0[q] = start;
-                hmax = max(hmax, int(start - (c * n1 + (n1 - s0) - 1)));
-                carry[q] = ld_pair(src + int64_t(__ldg(a.gather + start)) * ld);
-            }
-#pragma unroll 1
-            for (int h = 1; h <= hmax; ++h) {
-#pragma unroll
-                for (int q = 0; q < kQ; ++q) {
-                    const int c = u + 128 * q;
-                    const int32_t jj = j0[q] - h;
-                    if (jj < c * n1 + (n1 - s0) - 1) continue;  // past this chunk's non-storing steps
-                    const double2 x = ld_pair(src + int64_t(__ldg(a.gather + jj)) * ld);
-                    const double2 cs = __ldg(a.rec + 3 * int64_t(jj));
-                    carry[q] = make_double2(__dadd_rn(__dmul_rn(cs.x, x.x), __dmul_rn(cs.y, carry[q].x)),
-                                            __dadd_rn(__dmul_rn(cs.x, x.y), __dmul_rn(cs.y, carry[q].y)));
-                }
+                carry[q] = a.carries[int64_t(seg == 0 ? c : kN + c) * a.ldc + crow];
             }
         }
         // ---- values(0) straight from the step-0 index row; PRM(0) + IDX(1), Z(0) by TMA
@@ -312,6 +294,31 @@ __global__ void __launch_bounds__(kThreads, 1) p2fa_kernel(const P2faArgs a) {
     }
 }
 
+// The restart prologues of the fused pass as a separate, fully parallel pass: for every row
+// and chain boundary k (k < 1024: chunk k's own upper end; k >= 1024: the midpoint of chunk
+// k - 1024, where a split row block's second segment starts) the carry hchain_kernel would hold
+// there -- carry = x_start, then the non-storing steps j = start-1 .. B-1 in its operand order.
+// A warp is 32 consecutive rows of one boundary (512-byte gathers).  Replaces ~70 dependent
+// gather steps per chunk at the start of every fused-pass unit.
+__global__ void __launch_bounds__(256) p2fa_carry_kernel(const P2faArgs a, double2* __restrict__ carries) {
+    const int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int k = int(blockIdx.y);
+    if (row >= a.rows) return;
+    const int n1 = a.n1;
+    const int c = k < kN ? k : k - kN;
+    const int32_t start = k < kN ? __ldg(a.halo + c) : __ldg(a.halo_seg + 2 * c);
+    const int64_t last = k < kN ? int64_t(c + 1) * n1 - 1 : int64_t(c) * n1 + n1 / 2 - 1;  // B - 1
+    const double2* src = a.x1 + row;
+    double2 carry = src[int64_t(__ldg(a.gather + start)) * a.ld];
+    for (int64_t j = int64_t(start) - 1; j >= last; --j) {
+        const double2 x = src[int64_t(__ldg(a.gather + j)) * a.ld];
+        const double2 cs = __ldg(a.rec + 3 * j);
+        carry = make_double2(__dadd_rn(__dmul_rn(cs.x, x.x), __dmul_rn(cs.y, carry.x)),
+                             __dadd_rn(__dmul_rn(cs.x, x.y), __dmul_rn(cs.y, carry.y)));
+    }
+    carries[int64_t(k) * a.ldc + row] = carry;
+}
+
 // Step-major tables of one operator: rec_t[s][c] = {cs_j, d_{j+1}}, idx_t[s][c] = gather[j]
 // for j = n1 c + n1 - 2 - s (zeros where j < 0).
 __global__ void build_p2fa_tables_kernel(const double2* __restrict__ rec, const int32_t* __restrict__ gather, int n1,
@@ -350,6 +357,13 @@ void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, int n1
 // n = n1 x 1024 with pass A of length n2 = 1024 over the chunks and chain chunks of n1 indices
 bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows) {
     return n2 == kN && (n1 == 1024 || n1 == 3072) && n == n1 * n2 && rows > 0 && rows % 8 == 0;
+}
+
+void launch_p2fa_carries(const P2faArgs& a, double2* carries, cudaStream_t stream) {
+    const int64_t nrb = a.rows / 8;
+    const int nb = std::min(a.full_rb, nrb) < nrb ? 2 * kN : kN;  // midpoints only when row blocks split
+    p2fa_carry_kernel<<<dim3(ceil_div(a.rows, 256), unsigned(nb)), 256, 0, stream>>>(a, carries);
+    MNB_LAUNCH_CHECK();
 }
 
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream) {

@@ -61,6 +61,8 @@ struct P2faArgs {
     const int32_t* halo_seg = nullptr; // restart index per (n1 / 2)-index sub-chunk (split row blocks)
     int64_t full_rb = 1 << 30;       // row blocks run whole; the rest run as two k1 segments
     int n1 = 1024;                   // chain chunk = k1 steps per row block
+    const double2* carries = nullptr; // chain carries at the segment bounds [2048][ldc] (launch_p2fa_carries)
+    int64_t ldc = 0;
     int sync_mask = 15;              // cluster barrier every sync_mask + 1 steps (power of two; 16 measured best)
     const double2* tw = nullptr;     // w_1024^q
     const double2* rec_t = nullptr;  // step-major {cs_j, d_{j+1}} [n1 s][1024 c] (build_p2fa_tables)
@@ -71,6 +73,9 @@ struct P2faArgs {
 };
 bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows);
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream);
+// the restart prologues of launch_p2fa: carries[k * a.ldc + row] for the 1024 chunk ends (and the
+// 1024 chunk midpoints when row blocks split); a.carries / a.ldc must point at this buffer
+void launch_p2fa_carries(const P2faArgs& a, double2* carries, cudaStream_t stream);
 void build_p2fa_tables(const double2* rec, const int32_t* gather, int n1, double2* rec_t, int32_t* idx_t,
                        cudaStream_t stream);
 void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, int n1, double2* z_t, cudaStream_t stream);

@@ -509,7 +509,12 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             a.z_t = FP.p2fa_z.as<double2>();
             a.out = x2;
             a.rows = rs;
+            a.ldc = (rs + 7) & ~int64_t(7);
+            double2* carries = static_cast<double2*>(ctx.ws_carry.ensure(size_t(2 * 1024) * size_t(a.ldc) * 16));
+            a.carries = carries;
+            launch_p2fa_carries(a, carries, ctx.stream);
             launch_p2fa(a, ctx.num_sms, ctx.stream);
+            ctx.launches += 1;
             ctx.launches += 1;
             t.stop();
         } else {  // P2: Pi, Theta, then D (src/srft.cpp:56-57,128)

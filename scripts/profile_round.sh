@@ -8,7 +8,7 @@ B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
 timeout 900 ncu --nvtx --nvtx-include "solve/" --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof_$tag/launches_c4.csv $B > gpurun_out/prof_$tag/ncu_launch.log 2>&1
 python scripts/launch_summary.py gpurun_out/prof_$tag/launches_c4.csv > gpurun_out/prof_$tag/launches_c4_summary.txt 2>&1
-for k in pcg_pass_kernel hchain_kernel p2fa_kernel fft1024_select_kernel; do
+for k in pcg_pass_kernel hchain_kernel p2fa_kernel fft1024_select_kernel p2fa_carry_kernel; do
   timeout 900 ncu --nvtx --nvtx-include "solve/" --set full --clock-control none --import-source on \
     -k regex:$k -c 2 -o /tmp/${k}_$tag -f $B > gpurun_out/prof_$tag/ncu_${k}.log 2>&1
   python scripts/ncu_summary.py /tmp/${k}_$tag.ncu-rep > gpurun_out/prof_$tag/ncu_${k}_summary.txt 2>&1

@@ -54,6 +54,7 @@ void init_context(mnb::Context& c, int device) {
     if (const char* q = std::getenv("MNB_QR")) c.cholqr = std::string(q) != "householder";
     if (const char* q = std::getenv("MNB_CSNE")) c.csne = std::string(q) != "0";
     if (const char* q = std::getenv("MNB_P2FA")) c.p2fa = std::string(q) != "0";
+    if (const char* q = std::getenv("MNB_PRECOND_2NORM")) c.two_norm_check = std::string(q) != "0";
     if (cublasCreate(&c.cublas) != CUBLAS_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cublasCreate failed");
     cublasSetStream(c.cublas, c.stream);
     if (cusolverDnCreate(&c.cusolver) != CUSOLVER_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cusolverDnCreate failed");

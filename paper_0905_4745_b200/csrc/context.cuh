@@ -125,6 +125,7 @@ struct Context {
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
     bool p2fa = true;    // fused P2 + FFT pass A (k_p2fa.cu) where the shape allows; MNB_P2FA=0 disables
+    bool two_norm_check = true;  // one-pass preconditioner accepted on a 2-norm cond estimate; MNB_PRECOND_2NORM=0 disables
     bool csne = true;    // Step 2 from R1 = chol(S^H S) + corrected seminormal equations; MNB_CSNE=0 disables
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
     DevBuf Rinv, Rinv_rows;

@@ -272,3 +272,25 @@ def test_fused_tail_split_and_unfused_agree_at_scale(monkeypatch):
     torch.cuda.empty_cache()
     assert rel(out["split"], out["unfused"]) <= 1e-13
     assert rel(out["whole"], out["unfused"]) <= 1e-13
+
+
+def test_two_norm_preconditioner_check_matches_full_qr(monkeypatch):
+    """The one-pass preconditioner accepted on the 2-norm cond estimate (path 3 where the
+    Frobenius bound alone rejects, kappa = 1e6) gives the same solve as the full CholeskyQR2
+    preconditioner (MNB_PRECOND_2NORM=0): x within the solve tolerance, iterations +-1."""
+    m, n, kappa, eps = 256, 16384, 1e6, 1e-10
+    A, b = make_instance(m, n, kappa, seed=77)
+    cfg = mn.SolverConfig(epsilon=eps, seed=42)
+    reps = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MNB_PRECOND_2NORM", flag)
+        c = mn.Context(0)
+        reps[flag] = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        c.close()
+    a, f = reps["1"], reps["0"]
+    assert (f.extra["qr_path"] >> 4) in (0, 3)
+    assert (a.extra["qr_path"] >> 4) in (0, 3)
+    p = O.solve_classical(A, b)
+    assert rel(a.x, p) <= solve_tol(eps, kappa)
+    assert rel(a.x, f.x) <= solve_tol(eps, kappa)
+    assert abs(a.lsq_iterations - f.lsq_iterations) <= 1

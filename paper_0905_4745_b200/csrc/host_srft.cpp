@@ -2,6 +2,9 @@
 // seeded draws; see host_srft.hpp).  Compiled by the host C++ compiler with
 // -ffp-contract=off so every draw rounds exactly like src/rng.cpp.
 #include "host_srft.hpp"
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <atomic>
@@ -342,6 +345,7 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     if (n < 2) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: n must be at least 2");
     if (l < 1 || l > n) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: need 1 <= l <= n");
     if (n >= (int64_t(1) << 31)) throw Error(MNB_ERR_UNSUPPORTED, "build_srft: n must be below 2^31");
+    const auto t_build0 = std::chrono::steady_clock::now();
     if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
     op.n = n;
     op.l = l;
@@ -400,6 +404,9 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     std::atomic<bool> failed{false};
     std::exception_ptr error;
     std::mutex error_mu;
+    static const bool tr_tasks = std::getenv("MNB_TRACE") != nullptr;
+    double t_task[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::atomic<double> t_sincos_end{0.0};
     auto worker = [&] {
         try {
             for (int t; (t = next_draw.fetch_add(1)) < 8;) {
@@ -416,11 +423,18 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
                     case 6: angles_into(stream.substream(kZeta), zeta, n, 2); drawn[1] = 1; break;
                     case 7: angles_into(stream.substream(kD), d, n, 2); drawn[0] = 1; break;
                 }
+                if (tr_tasks) t_task[t] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                                                   t_build0).count();
             }
             for (int k : {4, 3, 2, 1, 0}) {
                 while (!drawn[k].load() && !failed.load()) std::this_thread::yield();
                 if (failed.load()) return;
                 for (int64_t b; (b = next_blk[k].fetch_add(1)) < nb;) sincos_block(k, b * blk);
+            }
+            if (tr_tasks) {
+                const double te = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_build0).count();
+                double cur = t_sincos_end.load();
+                while (te > cur && !t_sincos_end.compare_exchange_weak(cur, te)) {}
             }
         } catch (...) {
             std::lock_guard<std::mutex> g(error_mu);
@@ -435,7 +449,18 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         WorkerPool::get().run(nt, work);
     }
     if (error) std::rethrow_exception(error);
+    static const bool tr = std::getenv("MNB_TRACE") != nullptr;
+    const auto t_drawn = std::chrono::steady_clock::now();
     op.derive();
+    if (tr) {
+        const double ms_draw = std::chrono::duration<double, std::milli>(t_drawn - t_build0).count();
+        const double ms_derive =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_drawn).count();
+        std::fprintf(stderr, "[mnb] build_srft n=%lld threads=%d: draw %.2f ms, derive %.2f ms; tasks done at perm %.2f "
+                             "perm~ %.2f sample %.2f angles %.2f %.2f %.2f %.2f %.2f, last sincos %.2f ms\n",
+                     (long long)n, threads, ms_draw, ms_derive, t_task[0], t_task[1], t_task[2], t_task[3], t_task[4],
+                     t_task[5], t_task[6], t_task[7], t_sincos_end.load());
+    }
 }
 
 }  // namespace mnb

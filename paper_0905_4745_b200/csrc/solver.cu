@@ -893,7 +893,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     } else {
         upload_srft(ctx, T, Td);
         ctx.nonfinite = nonfinite;
-    trace("upload T");
+        trace("upload T issued");
         sketch_matrix(ctx, Td, Sbuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
         ctx.nonfinite = nullptr;
         MNB_CUDA(cudaEventRecord(eS, s1));

@@ -413,6 +413,9 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         const int64_t round_rows = 8 * int64_t(ctx.num_sms / 2);
         if (ms < rows && ctx.p2fa && !fp0.single && p2fa_supported(n, fp0.n1, fp0.n2, 8) && ms >= round_rows)
             ms = ms / round_rows * round_rows;
+        // MNB_SLAB_ROWS: force a smaller slab (tests of the multi-slab path at small m)
+        if (const char* e = std::getenv("MNB_SLAB_ROWS"))
+            if (const int64_t f = std::atoll(e); f > 0) ms = std::min<int64_t>(ms, std::max<int64_t>(8, f & ~int64_t(7)));
         sc = {n, rows, h.l, ctx.m, std::max<int64_t>(1, std::min<int64_t>(ms, rows))};
     }
     const int64_t Ms = sc.Ms;

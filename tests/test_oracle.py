@@ -343,3 +343,21 @@ def test_solver_tau_and_errors():
         O.solve_randomized(A, b, sketch_size=8, epsilon=2.0)
     with pytest.raises(O.ConfigError):
         O.solve_randomized(A, b, sketch_size=8, alpha=1.0)
+
+
+@pytest.mark.parametrize("real", [False, True])
+def test_exact_minnorm_against_svd_and_pivoted_qr(real):
+    """The extended-precision exact p (oracle.exact_minnorm, the yardstick of the full-size
+    parity campaign) agrees with the reference's SVD oracle (src/solver.cpp:148-156) at a
+    well-conditioned desk size, and at kappa = 1e6 it sits far below the float64 floor: the
+    pivoted-QR solution (src/solver.cpp:130-146) is ~u*kappa away from it, not more."""
+    A, b = make_instance(64, 1024, 10.0, seed=211, real=real)
+    p, hist = O.exact_minnorm(A, b)
+    assert np.linalg.norm(p - O.solve_svd(A, b)) <= 1e-14 * np.linalg.norm(p)
+    assert hist[-1] <= 1e-15
+    A, b = make_instance(128, 8192, 1e6, seed=212, real=real)
+    p, _ = O.exact_minnorm(A, b)
+    p2, _ = O.exact_minnorm(A, b, chunk=1000)  # chunking / threading does not change the answer
+    assert np.linalg.norm(p - p2) <= 1e-13 * np.linalg.norm(p)
+    e_qr = np.linalg.norm(O.solve_classical(A, b) - p) / np.linalg.norm(p)
+    assert 1e-13 < e_qr <= 10 * O.EPS * 1e6

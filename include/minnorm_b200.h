@@ -56,7 +56,9 @@ typedef struct mnb_context mnb_context;
 int mnb_context_create(int device, mnb_context** out);
 /* Column-sharded multi-GPU context: one process per GPU, NCCL communicator
  * built from a 128-byte ncclUniqueId that rank 0 created with
- * mnb_nccl_unique_id() and the launcher broadcast. */
+ * mnb_nccl_unique_id() and the launcher broadcast.  world_size 1 is allowed and
+ * takes the distributed code path (all-to-all, allgather, per-iteration
+ * allreduce) over a one-rank communicator. */
 int mnb_nccl_unique_id(void* out128);
 int mnb_context_create_distributed(int device, int rank, int world_size, const void* nccl_unique_id,
                                    mnb_context** out);
@@ -65,6 +67,18 @@ void mnb_context_destroy(mnb_context* ctx);
 int mnb_context_set_stream(mnb_context* ctx, void* cuda_stream);
 /* Column partition used by every multi-GPU entry point (pure host logic). */
 int mnb_shard_columns(int64_t n, int world_size, int rank, int64_t* col_begin, int64_t* col_count);
+/* The distributed sketch's one all-to-all (column shards -> row blocks; pure host logic, the
+ * table the CUDA path itself follows).  For every peer h = 0..world_size-1 of `rank`, six
+ * entries at plan[6h..6h+5]:
+ *   send_row0, send_rows  rows of A that rank h owns (mnb_shard_columns(m, world, h));
+ *   send_offset           element offset of block h in the pack buffer: block h is
+ *                         A[send_row0 : +send_rows, this rank's columns], column-major, ld send_rows;
+ *   recv_col0, recv_cols  columns rank h owns (mnb_shard_columns(n_global, world, h));
+ *   recv_offset           element offset (recv_col0 * my_rows) in this rank's row block, which is
+ *                         my_rows x n_global, column-major, ld my_rows.
+ * Replaces the reference's serial column loop over B = A^* (src/srft.cpp:147-153) being cut
+ * into row blocks; there is no reference counterpart (single process). */
+int mnb_redistribute_plan(int64_t m, int64_t n_global, int world_size, int rank, int64_t* plan);
 
 /* The problem matrix A (ProblemInstance::A, include/minnorm/solver.hpp:14-24):
  * this rank's column shard A[:, col_begin : col_begin+n_local], column-major

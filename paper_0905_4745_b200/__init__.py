@@ -8,12 +8,12 @@ small QR, NCCL for column-sharded multi-GPU runs.
 """
 from .api import (apply_adjoint_matrix, ConfigError, Context, DeviceError, DimensionError, LsqConfig, LsqSolution, ProblemInstance,
                   RankDeficiencyError, Sampling, SolveReport, SolverConfig, SrftOperator, UnsupportedError,
-                  build_srft, default_context, derive_seed, dft, idft, shard_columns, solve_classical,
+                  build_srft, default_context, derive_seed, dft, idft, redistribute_plan, shard_columns, solve_classical,
                   solve_least_squares, solve_randomized, srft_from_fields, ClassicalReport)
 
 __all__ = [
     "apply_adjoint_matrix", "ConfigError", "Context", "DeviceError", "DimensionError", "LsqConfig", "LsqSolution", "ProblemInstance",
     "RankDeficiencyError", "Sampling", "SolveReport", "SolverConfig", "SrftOperator", "UnsupportedError",
-    "build_srft", "default_context", "derive_seed", "dft", "idft", "shard_columns", "solve_classical",
+    "build_srft", "default_context", "derive_seed", "dft", "idft", "redistribute_plan", "shard_columns", "solve_classical",
     "solve_least_squares", "solve_randomized", "srft_from_fields", "ClassicalReport",
 ]

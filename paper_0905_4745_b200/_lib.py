@@ -72,6 +72,7 @@ class LsqSolutionC(ctypes.Structure):
 EXPORTS = [
     "mnb_last_error", "mnb_last_deficient_columns", "mnb_version", "mnb_context_create", "mnb_nccl_unique_id",
     "mnb_context_create_distributed", "mnb_context_destroy", "mnb_context_set_stream", "mnb_shard_columns",
+    "mnb_redistribute_plan",
     "mnb_set_matrix", "mnb_solver_config_default", "mnb_solve_randomized", "mnb_solve_classical",
     "mnb_solve_least_squares",
     "mnb_srft_build", "mnb_srft_from_fields", "mnb_srft_destroy", "mnb_srft_get_field", "mnb_srft_dims",
@@ -111,6 +112,7 @@ def load():
     L.mnb_context_destroy.restype = None
     L.mnb_context_set_stream.argtypes = [vp, vp]
     L.mnb_shard_columns.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.mnb_redistribute_plan.argtypes = [i64, i64, ci, ci, ctypes.POINTER(i64)]
     L.mnb_set_matrix.argtypes = [vp, ci, i64, i64, i64, i64, dp, i64, ci]
     L.mnb_solver_config_default.argtypes = [ctypes.POINTER(SolverConfigC)]
     L.mnb_solver_config_default.restype = None

@@ -116,6 +116,7 @@ class Context:
         self._h = _handle
         self.device = device
         self.rank, self.world_size = 0, 1
+        self.is_distributed = False
         self.m = self.n = self.col_begin = self.n_local = 0
         self.dtype = None
 
@@ -133,7 +134,21 @@ class Context:
         _check(lib.mnb_context_create_distributed(device, rank, world_size, uid, ctypes.byref(h)))
         ctx = cls(device, _handle=h)
         ctx.rank, ctx.world_size = rank, world_size
+        ctx.is_distributed = True
         return ctx
+
+    def set_shard(self, A, n_global: Optional[int] = None) -> None:
+        """Distributed context: A is this rank's column shard of an m x n_global matrix, the
+        columns mnb_shard_columns(n_global, world_size, rank) assigns.  n_global defaults to the
+        one of the last set_matrix call; a shard whose width does not match is a DimensionError."""
+        n_global = int(n_global or self.n)
+        if n_global <= 0:
+            raise ValueError("distributed context: pass n_global (the global column count) with the first shard")
+        col_begin, count = shard_columns(n_global, self.world_size, self.rank)
+        if A.shape[1] != count:
+            raise DimensionError(f"rank {self.rank} of {self.world_size}: shard has {A.shape[1]} columns, "
+                                 f"mnb_shard_columns({n_global}) assigns {count}")
+        self.set_matrix(A, n_global=n_global, col_begin=col_begin)
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -210,6 +225,16 @@ def shard_columns(n: int, world_size: int, rank: int) -> tuple[int, int]:
     return b.value, c.value
 
 
+def redistribute_plan(m: int, n_global: int, world_size: int, rank: int) -> np.ndarray:
+    """The distributed sketch's all-to-all table (mnb_redistribute_plan): one row per peer h,
+    [send_row0, send_rows, send_offset, recv_col0, recv_cols, recv_offset] (offsets in elements
+    of the pack buffer / of this rank's my_rows x n_global column-major row block)."""
+    plan = np.zeros((world_size, 6), np.int64)
+    _check(L.load().mnb_redistribute_plan(int(m), int(n_global), int(world_size), int(rank),
+                                          plan.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+    return plan
+
+
 # ----------------------------------------------------------------- solver --
 @dataclass
 class SolverConfig:
@@ -281,23 +306,23 @@ class ProblemInstance:
 
 
 def solve_randomized(inst: ProblemInstance, cfg: SolverConfig = SolverConfig(), ctx: Optional[Context] = None,
-                     x_out=None, c_out=None) -> SolveReport:
+                     x_out=None, c_out=None, n_global: Optional[int] = None) -> SolveReport:
     """solve_randomized (include/minnorm/solver.hpp:55; src/solver.cpp:50-128) on the GPU.
 
-    With a multi-GPU context, `inst.A` is this rank's column shard and the
-    returned x / c are this rank's entries."""
+    With a distributed context, `inst.A` is this rank's column shard (Context.set_shard:
+    n_global is required with the first shard) and the returned x / c are this rank's entries."""
     ctx = ctx or default_context()
     A = inst.A
     if A is not None:
         if len(inst.b) != A.shape[0]:
             raise DimensionError(f"right-hand side length {len(inst.b)} does not match m={A.shape[0]}")
-        if ctx.world_size == 1:
+        if not ctx.is_distributed:
             if A.shape[0] < 1 or A.shape[0] >= A.shape[1]:
                 raise DimensionError(f"problem must be underdetermined: 1 <= m < n, got m={A.shape[0]}, "
                                      f"n={A.shape[1]}")
             ctx.set_matrix(A, deferred=True)  # pinned host A: copied in slabs under the sketches
         else:
-            ctx.set_matrix(A, n_global=ctx.n, col_begin=ctx.col_begin)
+            ctx.set_shard(A, n_global)
     b = _host_c128(inst.b.cpu().numpy() if _is_torch_cuda(inst.b) else inst.b)
     rc = L.SolveReportC()
     if x_out is not None:  # device tensors (torch), zero-copy
@@ -352,7 +377,8 @@ class ClassicalReport:
     seconds: float
 
 
-def solve_classical(inst: ProblemInstance, ctx: Optional[Context] = None, report: bool = False):
+def solve_classical(inst: ProblemInstance, ctx: Optional[Context] = None, report: bool = False,
+                    n_global: Optional[int] = None):
     """solve_classical (include/minnorm/solver.hpp:59; src/solver.cpp:130-146) on the GPU:
     the minimal-norm x of A x = b by the deterministic O(m^2 n) method (the paper's t0
     baseline).  Returns x (this rank's entries), or (x, ClassicalReport) with report=True.
@@ -362,10 +388,10 @@ def solve_classical(inst: ProblemInstance, ctx: Optional[Context] = None, report
     if A is not None:
         if len(inst.b) != A.shape[0]:
             raise DimensionError(f"right-hand side length {len(inst.b)} does not match m={A.shape[0]}")
-        if ctx.world_size == 1:
+        if not ctx.is_distributed:
             ctx.set_matrix(A)
         else:
-            ctx.set_matrix(A, n_global=ctx.n, col_begin=ctx.col_begin)
+            ctx.set_shard(A, n_global)
     b = _host_c128(inst.b.cpu().numpy() if _is_torch_cuda(inst.b) else inst.b)
     x = np.zeros(ctx.n_local, np.complex128)
     rc = L.ClassicalReportC()

@@ -99,6 +99,14 @@ int mnb_context_create(int device, mnb_context** out) {
     });
 }
 
+int mnb_redistribute_plan(int64_t m, int64_t n_global, int world_size, int rank, int64_t* plan) {
+    return guard([&] {
+        mnb::require(world_size >= 1 && rank >= 0 && rank < world_size && m >= 1 && n_global >= 1 && plan,
+                     MNB_ERR_INVALID_ARGUMENT, "mnb_redistribute_plan: bad arguments");
+        mnb::redistribute_plan(m, n_global, world_size, rank, plan);
+    });
+}
+
 int mnb_nccl_unique_id(void* out128) {
     return guard([&] {
         static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -116,11 +124,9 @@ int mnb_context_create_distributed(int device, int rank, int world_size, const v
             init_context(c->ctx, device);
             c->ctx.rank = rank;
             c->ctx.world = world_size;
-            if (world_size > 1) {
-                ncclUniqueId id;
-                std::memcpy(&id, nccl_unique_id, sizeof id);
-                nccl_ok(ncclCommInitRank(&c->ctx.comm, world_size, id, rank), "ncclCommInitRank");
-            }
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_unique_id, sizeof id);
+            nccl_ok(ncclCommInitRank(&c->ctx.comm, world_size, id, rank), "ncclCommInitRank");
         } catch (...) {
             delete c;
             throw;
@@ -156,7 +162,8 @@ int mnb_set_matrix(mnb_context* ctx, int dtype, int64_t m, int64_t n_global, int
         mnb::require(m >= 1 && n_global >= 1 && n_local >= 0 && col_begin >= 0 && col_begin + n_local <= n_global,
                      MNB_ERR_DIMENSION, "mnb_set_matrix: inconsistent dimensions");
         mnb::require(lda >= m, MNB_ERR_INVALID_ARGUMENT, "mnb_set_matrix: lda < m");
-        if (c.world > 1) {
+        c.slab_ready = false;
+        if (c.distributed()) {
             int64_t b = 0, cnt = 0;
             mnb_shard_columns(n_global, c.world, c.rank, &b, &cnt);
             mnb::require(b == col_begin && cnt == n_local, MNB_ERR_DIMENSION,
@@ -178,7 +185,7 @@ int mnb_set_matrix(mnb_context* ctx, int dtype, int64_t m, int64_t n_global, int
         void* dst = c.A_own.ensure(std::max<size_t>(size_t(m) * size_t(n_local) * out_esz, 16));
         c.pending_host = false;
         c.A_host = nullptr;
-        if (location == MNB_HOST_ASYNC && c.world == 1 && !promote && n_local > 0) {
+        if (location == MNB_HOST_ASYNC && !c.distributed() && !promote && n_local > 0) {
             cudaPointerAttributes attr{};
             const bool pinned = cudaPointerGetAttributes(&attr, A) == cudaSuccess && attr.type == cudaMemoryTypeHost;
             cudaGetLastError();
@@ -412,6 +419,7 @@ int mnb_srft_apply_to_columns(mnb_context* ctx, const mnb_srft* op, void* out, i
         const size_t bytes = size_t(op->host.l) * size_t(c.m) * 16;
         double2* S = out_location == MNB_DEVICE ? static_cast<double2*>(out)
                                                 : static_cast<double2*>(c.sk_S.ensure(bytes));
+        c.slab_ready = false;  // the matrix may have changed in place since the last exchange
         mnb::sketch_matrix(c, dev, S, nullptr, nullptr);
         if (out_location != MNB_DEVICE) copy_out(out, S, bytes, MNB_HOST, c.stream);
         mnb::sync(c);

@@ -102,8 +102,9 @@ struct Context {
     cublasHandle_t cublas = nullptr;
     cusolverDnHandle_t cusolver = nullptr;
     cusolverDnParams_t cusolver_params = nullptr;
-    ncclComm_t comm = nullptr;
+    ncclComm_t comm = nullptr;  // set by mnb_context_create_distributed (any world size, 1 included)
     int rank = 0, world = 1;
+    bool distributed() const { return comm != nullptr; }
 
     // problem matrix (this rank's column shard)
     int dtype = MNB_C128;
@@ -121,6 +122,10 @@ struct Context {
 
     // workspaces
     DevBuf ws_x1, ws_x2, ws_slab, ws_pack, ws_carry;
+    // distributed: this rank's row block of A after the all-to-all (redistribute_rows), valid
+    // until the matrix changes or the next solve starts
+    bool slab_ready = false;
+    int64_t slab_rows = 0, slab_row0 = 0;
     DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
@@ -163,7 +168,11 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev);
 // T * conj(rows [row0,row0+rows) of a column-major block) -> out[slot + (out_row0 + r) * ldo]
 void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real, int64_t lda, int64_t row0,
                   int64_t rows, double2* out, int64_t ldo, int64_t out_row0, double* kernel_ms);
-// Full sketch of the context matrix (multi-GPU: all-to-all + allgather): out l x m col-major (device).
+// The sketch all-to-all's table (see mnb_redistribute_plan) and the exchange itself.
+void redistribute_plan(int64_t m, int64_t n_global, int world, int rank, int64_t* plan);
+void redistribute_rows(Context& ctx, double* seconds);
+// Full sketch of the context matrix (distributed: local rows of the redistributed slab +
+// allgather; the all-to-all runs first if this solve has not done it): out l x m col-major (device).
 void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel_ms, double* redistribute_s);
 // T^* v for one device vector v (l) -> y (n, device).
 void srft_adjoint_vec(Context& ctx, const SrftDev& op, const double2* v, double2* y);

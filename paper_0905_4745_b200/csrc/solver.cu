@@ -80,7 +80,8 @@ int64_t deficient_count(Context& ctx, const double2* QR, int64_t ld, int64_t m, 
 }
 
 void allreduce_sum(Context& ctx, double* buf, size_t count) {
-    if (ctx.world > 1) nccl_check(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm, ctx.stream), "ncclAllReduce");
+    if (ctx.distributed())
+        nccl_check(ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, ctx.comm, ctx.stream), "ncclAllReduce");
 }
 
 struct PassBuffers {
@@ -252,6 +253,7 @@ void launch_cg_init_from_sketch(Context& ctx, const double2* S, int64_t l, const
     launch_sketch_adjoint_gemv(S, l, m, z, reinterpret_cast<double2*>(pb.red), ctx.stream);
     launch_cg_init_vectors(c, n, r, t, x, part, parts, pb.red + 2 * m, ctx.stream);
     ctx.launches += 3;
+    allreduce_sum(ctx, pb.red + 2 * m, 4);  // ||c||^2 over the ranks' columns (S^H z is already global)
     MNB_CUDA(cudaEventRecord(ctx.event(21), ctx.stream));
     ctx.init_from_sketch = true;
 }
@@ -784,7 +786,8 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     // Deferred host A (MNB_HOST_ASYNC, one GPU): copy it in row slabs on a side stream now; both
     // sketches then run slab by slab as the rows land, so the H2D hides the parameter draws, the
     // sketches and most of Step 1.  Otherwise A is already resident.
-    const bool pipelined = ctx.pending_host && ctx.world == 1 && ctx.n_local > 0;
+    const bool pipelined = ctx.pending_host && !ctx.distributed() && ctx.n_local > 0;
+    ctx.slab_ready = false;  // distributed: this solve's one all-to-all feeds both sketches
     std::vector<std::pair<int64_t, int64_t>> slabs;  // (row0, rows)
     if (!pipelined) ctx.make_resident();
     // T (needed first) is drawn with every host thread; T' is drawn in the background with half
@@ -855,15 +858,16 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         fut_Tp = host_async([&] { build_Tp(std::max(1, hw / 2)); });
     }
 
-    // Streams: the sketches and the CG passes (memory-bound) run on ctx.stream; with one GPU the
-    // QRs and Steps 2-3 (tensor-core / latency-bound) run on an auxiliary stream beside them:
+    // Streams: the sketches and the CG passes (memory-bound) run on ctx.stream; the QRs and
+    // Steps 2-3 (tensor-core / latency-bound) run on an auxiliary stream beside them:
     //   s1: sketch S | sketch E | INIT pass (after c) | CG (after R')
     //   s2:          | QR(S), Step 2, Step 3 (c)      | QR(E)
-    const bool concurrent = ctx.world == 1;
+    // Every NCCL call (all-to-all, allgathers, the finiteness allreduce, the CG allreduces) is
+    // issued on s1 in the same host order on every rank; s2 carries none.
     trace("params done");
     cudaStream_t s1 = ctx.stream;
-    if (concurrent && !ctx.aux_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
-    cudaStream_t s2 = concurrent ? ctx.aux_stream : s1;
+    if (!ctx.aux_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
+    cudaStream_t s2 = ctx.aux_stream;
     int* nonfinite = dev<int>(ctx.flag, 1);
     double2* Sbuf = dev<double2>(ctx.sk_S, size_t(l) * size_t(m));
     double2* Ebuf = dev<double2>(ctx.sk_E, size_t(l) * size_t(m));
@@ -896,14 +900,15 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         trace("upload T issued");
         sketch_matrix(ctx, Td, Sbuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
         ctx.nonfinite = nullptr;
+        if (ctx.distributed())  // every rank flagged its own row block
+            nccl_check(ncclAllReduce(nonfinite, nonfinite, 1, ncclInt, ncclMax, ctx.comm, s1), "ncclAllReduce");
         MNB_CUDA(cudaEventRecord(eS, s1));
-        if (concurrent) {    trace("sketch S issued");
-  // E's sketch queues behind S's on s1 while s2 factors S
-            fut_Tp.get();
-            upload_srft(ctx, Tp, Tpd);
-            sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
-            MNB_CUDA(cudaEventRecord(eE, s1));
-        }
+        trace("sketch S issued");
+        // E's sketch queues behind S's on s1 (from the same redistributed slab) while s2 factors S
+        fut_Tp.get();
+        upload_srft(ctx, Tp, Tpd);
+        sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+        MNB_CUDA(cudaEventRecord(eE, s1));
     }
     trace("sketch E issued");
 
@@ -920,11 +925,6 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
         MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
         sync(ctx);
-        if (ctx.world > 1) {
-            nccl_check(ncclAllReduce(nonfinite, nonfinite, 1, ncclInt, ncclMax, ctx.comm, ctx.stream), "ncclAllReduce");
-            MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-            sync(ctx);
-        }
         if (flag) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
         rep.step_seconds[0] = now_s() - t0;
 
@@ -960,12 +960,6 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
 
     // ---- Step 4: y = argmin ||A^* y - c||  (src/solver.cpp:104-114, src/lsq.cpp:43-113)
     t0 = now_s();
-    if (!concurrent) {
-        fut_Tp.get();
-        upload_srft(ctx, Tp, Tpd);
-        sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
-        MNB_CUDA(cudaEventRecord(eE, s1));
-    }
     rep.param_seconds = t_param_T + t_param_Tp;
     double2* y = dev<double2>(ctx.vec_m[5], size_t(m));
     double2* ax = dev<double2>(ctx.vec_m[7], size_t(m));
@@ -973,7 +967,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     // the INIT pass (r = c, s = A c) needs only c: on s1 while s2 factors E
     MNB_CUDA(cudaStreamWaitEvent(s1, eC, 0));
     // (A c = S^H z needs the sketch intact: not after the Householder fallback, which overwrote it)
-    if (concurrent && sq.path != 2 && !std::getenv("MNB_INIT_PASS")) launch_cg_init_from_sketch(ctx, Sbuf, l, z, c_loc, xacc);
+    if (sq.path != 2 && !std::getenv("MNB_INIT_PASS")) launch_cg_init_from_sketch(ctx, Sbuf, l, z, c_loc, xacc);
     else launch_cg_init_pass(ctx, c_loc, xacc);
     trace("INIT issued");
     SketchQr eq;
@@ -1226,7 +1220,7 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
     }
     if (!ok) {
         // ---- path 1: Householder QR of A^H (n x m), x = Q [R^{-H} b; 0]
-        if (ctx.world > 1 || ctx.dtype != MNB_C128)
+        if (ctx.distributed() || ctx.dtype != MNB_C128)
             throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: A is too ill-conditioned for the Gram path and the "
                                              "Householder fallback runs on one GPU with complex A");
         double2* AH = dev<double2>(ctx.ws_x1, size_t(n) * size_t(m));

@@ -583,27 +583,41 @@ int shard_begin(int64_t n, int world, int rank, int64_t* count) {
     return 0;
 }
 
-void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel_ms, double* redistribute_s) {
-    const int64_t m = ctx.m, l = op.host->l;
-    const int is_real = ctx.dtype == MNB_F64;
-    if (ctx.world == 1) {
-        sketch_block(ctx, op, ctx.A, is_real, m, 0, m, out, l, 0, kernel_ms);
-        return;
+// The all-to-all of the multi-GPU sketch (north_star item 5), as one table per peer h
+// (mnb_redistribute_plan in include/minnorm_b200.h):
+//   [send_row0, send_rows, send_offset, recv_col0, recv_cols, recv_offset]
+// Rank h owns rows mnb_shard_columns(m, world, h) of A and columns mnb_shard_columns(n, world, h).
+// pack: block h = A[send_row0 : +send_rows, this rank's columns], column-major (ld send_rows),
+//       at element send_offset of the pack buffer;
+// slab: this rank's row block (my_rows x n_global, column-major, ld my_rows); peer h's
+//       columns land at element recv_offset = recv_col0 * my_rows.
+void redistribute_plan(int64_t m, int64_t n_global, int world, int rank, int64_t* plan) {
+    int64_t my_rows = 0, my_cols = 0, b = 0;
+    mnb_shard_columns(m, world, rank, &b, &my_rows);
+    mnb_shard_columns(n_global, world, rank, &b, &my_cols);
+    for (int h = 0; h < world; ++h) {
+        int64_t r0, rc, c0, cc;
+        mnb_shard_columns(m, world, h, &r0, &rc);
+        mnb_shard_columns(n_global, world, h, &c0, &cc);
+        int64_t* p = plan + 6 * size_t(h);
+        p[0] = r0;
+        p[1] = rc;
+        p[2] = r0 * my_cols;
+        p[3] = c0;
+        p[4] = cc;
+        p[5] = c0 * my_rows;
     }
-    // ---- all-to-all: column shards -> row blocks (north_star item 5) ----
+}
+
+// Column shards -> this rank's row block in ctx.ws_slab: one pack (2D copies) and one grouped
+// ncclSend/ncclRecv exchange.  Runs once per solve; both sketches (S and E) read the slab.
+void redistribute_rows(Context& ctx, double* seconds) {
+    const int64_t m = ctx.m;
     const size_t esz = ctx.esz();
-    std::vector<int64_t> rb(size_t(ctx.world) + 1, 0), cb(size_t(ctx.world) + 1, 0);
-    for (int h = 0; h < ctx.world; ++h) {
-        int64_t b, c;
-        mnb_shard_columns(m, ctx.world, h, &b, &c);
-        rb[size_t(h)] = b;
-        rb[size_t(h) + 1] = b + c;
-        mnb_shard_columns(ctx.n_global, ctx.world, h, &b, &c);
-        cb[size_t(h)] = b;
-        cb[size_t(h) + 1] = b + c;
-    }
+    std::vector<int64_t> plan(size_t(6 * ctx.world));
+    redistribute_plan(m, ctx.n_global, ctx.world, ctx.rank, plan.data());
     const int me = ctx.rank;
-    const int64_t mh = rb[size_t(me) + 1] - rb[size_t(me)];
+    const int64_t mh = plan[size_t(6 * me + 1)];
     cudaEvent_t e0 = ctx.event(10), e1 = ctx.event(11);
     MNB_CUDA(cudaEventRecord(e0, ctx.stream));
     unsigned char* pack = static_cast<unsigned char*>(ctx.ws_pack.ensure(size_t(m) * size_t(ctx.n_local) * esz + 16));
@@ -611,20 +625,19 @@ void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel
         static_cast<unsigned char*>(ctx.ws_slab.ensure(size_t(std::max<int64_t>(mh, 1)) * size_t(ctx.n_global) * esz + 16));
     const unsigned char* A = static_cast<const unsigned char*>(ctx.A);
     for (int h = 0; h < ctx.world; ++h) {
-        const int64_t rows = rb[size_t(h) + 1] - rb[size_t(h)];
-        if (rows == 0 || ctx.n_local == 0) continue;
-        unsigned char* dst = pack + size_t(rb[size_t(h)]) * size_t(ctx.n_local) * esz;
-        MNB_CUDA(cudaMemcpy2DAsync(dst, size_t(rows) * esz, A + size_t(rb[size_t(h)]) * esz, size_t(m) * esz,
-                                   size_t(rows) * esz, size_t(ctx.n_local), cudaMemcpyDeviceToDevice, ctx.stream));
+        const int64_t* p = &plan[size_t(6 * h)];
+        if (p[1] == 0 || ctx.n_local == 0) continue;
+        MNB_CUDA(cudaMemcpy2DAsync(pack + size_t(p[2]) * esz, size_t(p[1]) * esz, A + size_t(p[0]) * esz,
+                                   size_t(m) * esz, size_t(p[1]) * esz, size_t(ctx.n_local), cudaMemcpyDeviceToDevice,
+                                   ctx.stream));
     }
     nccl_check(ncclGroupStart(), "ncclGroupStart");
     for (int h = 0; h < ctx.world; ++h) {
-        const int64_t rows_h = rb[size_t(h) + 1] - rb[size_t(h)];
-        const int64_t cols_h = cb[size_t(h) + 1] - cb[size_t(h)];
-        unsigned char* send = pack + size_t(rb[size_t(h)]) * size_t(ctx.n_local) * esz;
-        unsigned char* recv = slab + size_t(cb[size_t(h)]) * size_t(mh) * esz;
-        const size_t send_d = size_t(rows_h) * size_t(ctx.n_local) * esz / 8;
-        const size_t recv_d = size_t(mh) * size_t(cols_h) * esz / 8;
+        const int64_t* p = &plan[size_t(6 * h)];
+        unsigned char* send = pack + size_t(p[2]) * esz;
+        unsigned char* recv = slab + size_t(p[5]) * esz;
+        const size_t send_d = size_t(p[1]) * size_t(ctx.n_local) * esz / 8;
+        const size_t recv_d = size_t(mh) * size_t(p[4]) * esz / 8;
         if (h == me) {
             if (send_d)
                 MNB_CUDA(cudaMemcpyAsync(recv, send, send_d * 8, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -635,24 +648,40 @@ void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel
     }
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+    ctx.slab_ready = true;
+    ctx.slab_rows = mh;
+    ctx.slab_row0 = plan[size_t(6 * me)];
+    if (seconds) {
+        MNB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *seconds += ms * 1e-3;
+    }
+}
+
+void sketch_matrix(Context& ctx, const SrftDev& op, double2* out, double* kernel_ms, double* redistribute_s) {
+    const int64_t m = ctx.m, l = op.host->l;
+    const int is_real = ctx.dtype == MNB_F64;
+    if (!ctx.distributed()) {
+        sketch_block(ctx, op, ctx.A, is_real, m, 0, m, out, l, 0, kernel_ms);
+        return;
+    }
+    if (!ctx.slab_ready) redistribute_rows(ctx, redistribute_s);
     // ---- local sketch of this rank's row block ----
-    if (mh > 0) sketch_block(ctx, op, slab, is_real, mh, 0, mh, out + rb[size_t(me)] * l, l, 0, kernel_ms);
+    const int64_t mh = ctx.slab_rows;
+    if (mh > 0)
+        sketch_block(ctx, op, ctx.ws_slab.p, is_real, mh, 0, mh, out + ctx.slab_row0 * l, l, 0, kernel_ms);
     // ---- allgather the sketch columns (every rank runs the replicated QR) ----
     nccl_check(ncclGroupStart(), "ncclGroupStart");
     for (int h = 0; h < ctx.world; ++h) {
-        const int64_t rows_h = rb[size_t(h) + 1] - rb[size_t(h)];
+        int64_t r0, rows_h;
+        mnb_shard_columns(m, ctx.world, h, &r0, &rows_h);
         if (!rows_h) continue;
-        double2* blk = out + rb[size_t(h)] * l;
+        double2* blk = out + r0 * l;
         nccl_check(ncclBroadcast(blk, blk, size_t(rows_h) * size_t(l) * 2, ncclDouble, h, ctx.comm, ctx.stream),
                    "ncclBroadcast");
     }
     nccl_check(ncclGroupEnd(), "ncclGroupEnd");
-    if (redistribute_s) {
-        MNB_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        MNB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        *redistribute_s += ms * 1e-3;
-    }
 }
 
 void dft_vec_to(Context& ctx, int64_t n, const double2* in, double2* out, bool inverse) {

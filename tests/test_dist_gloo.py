@@ -60,27 +60,35 @@ def _worker(rank, world, port, q):
         tr = torch.from_numpy(red.copy())
         dist.all_reduce(tr, op=dist.ReduceOp.SUM)
         red_all = tr.numpy()
-        # ---- the sketch all-to-all into row blocks
-        rows = [mn.shard_columns(m, world, h) for h in range(world)]
-        cols = [mn.shard_columns(n, world, h) for h in range(world)]
-        send = [torch.from_numpy(np.ascontiguousarray(AJ[rb:rb + rc, :]).view(np.float64).copy())
-                for rb, rc in rows]
-        recv = [torch.zeros(rows[rank][1] * cols[h][1] * 2, dtype=torch.float64) for h in range(world)]
+        # ---- the sketch all-to-all into row blocks, laid out by the library's own table
+        # (mnb_redistribute_plan: the offsets srft_gpu.cu redistribute_rows packs and receives at)
+        plan = mn.redistribute_plan(m, n, world, rank)
+        my_rows = int(plan[rank, 1])
+        pack = np.zeros(m * cn, np.complex128)
+        for h in range(world):
+            r0, rc, off = plan[h, 0], plan[h, 1], plan[h, 2]
+            pack[off:off + rc * cn] = AJ[r0:r0 + rc, :].ravel(order="F")  # column-major, ld rc
+        slab = np.zeros(my_rows * n, np.complex128)
+        send = [torch.from_numpy(pack[plan[h, 2]:plan[h, 2] + plan[h, 1] * cn].view(np.float64).copy())
+                for h in range(world)]
+        recv = [torch.zeros(my_rows * int(plan[h, 4]) * 2, dtype=torch.float64) for h in range(world)]
         # grouped point-to-point, as the CUDA path's ncclGroupStart/ncclSend/ncclRecv (srft_gpu.cu)
         ops = []
         for h in range(world):
             if h == rank:
-                recv[h].copy_(send[h].reshape(-1))
+                recv[h].copy_(send[h])
                 continue
-            ops.append(dist.P2POp(dist.isend, send[h].reshape(-1), h))
+            ops.append(dist.P2POp(dist.isend, send[h], h))
             ops.append(dist.P2POp(dist.irecv, recv[h], h))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        rb, rc = rows[rank]
-        block = np.zeros((rc, n), np.complex128, order="F")
         for h in range(world):
-            hb, hc = cols[h]
-            block[:, hb:hb + hc] = recv[h].numpy().view(np.complex128).reshape(rc, hc)
+            off, cnt = plan[h, 5], my_rows * plan[h, 4]
+            slab[off:off + cnt] = recv[h].numpy().view(np.complex128)
+        block = slab.reshape(n, my_rows).T  # my_rows x n, column-major (ld my_rows)
+        rows = [mn.shard_columns(m, world, h) for h in range(world)]
+        rb, rc = rows[rank]
+        assert (rb, rc) == (plan[rank, 0], my_rows)
         op = O.Srft.build(48, n, O.derive_seed(42, 11))
         S_local = op.sketch(block, threads=1)  # l x rc
         gathered = [torch.zeros(48 * rows[h][1] * 2, dtype=torch.float64) for h in range(world)]
@@ -95,7 +103,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_pass_and_sketch_redistribution_match_unsharded(world):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

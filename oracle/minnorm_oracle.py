@@ -548,6 +548,67 @@ def exact_minnorm(A: np.ndarray, b: np.ndarray, iters: int = 8, chunk: int = 1 <
     return p.astype(np.complex128), hist
 
 
+# ------------------------------------------------------- instance generator --
+@dataclass
+class GeneratedInstance:
+    """include/minnorm/bench.hpp (GeneratedInstance): A = U diag(sigma) V^H, b = A p_true."""
+    A: np.ndarray
+    b: np.ndarray
+    p_true: np.ndarray
+    kappa: float
+
+
+def _gaussian_matrix(stream_seed: int, rows: int, cols: int) -> np.ndarray:
+    """src/bench.cpp:18-23: complex_gaussian() draws in column-major order."""
+    return rng_draw(stream_seed, "complex_gaussian", rows * cols).reshape(cols, rows).T.copy()
+
+
+def _orthonormalize_columns(X: np.ndarray) -> np.ndarray:
+    """src/bench.cpp:26-37: modified Gram-Schmidt, two projection sweeps per column."""
+    X = X.copy()
+    for j in range(X.shape[1]):
+        v = X[:, j].copy()
+        for _ in range(2):
+            for i in range(j):
+                v -= np.vdot(X[:, i], v) * X[:, i]
+        nv = np.linalg.norm(v)
+        if not nv > 0.0:
+            raise RuntimeError("orthonormalize_columns: degenerate Gaussian draw")
+        X[:, j] = v / nv
+    return X
+
+
+def generate_instance(m: int, n: int, kappa: float, stream_seed: int) -> GeneratedInstance:
+    """src/bench.cpp:46-74 (tags 21/22/23 at :16): sigma_j = kappa^{-j/(m-1)}, p_true = V w with
+    w_j = sign/sqrt(m), b = A p_true.  `stream_seed` is the seed of the RandomStream passed in."""
+    if m < 2:
+        raise ValueError("generate_instance: m must be at least 2")
+    if m >= n:
+        raise ValueError("generate_instance: need m < n")
+    if not kappa >= 1.0:
+        raise ValueError("generate_instance: kappa must be >= 1")
+    U = _orthonormalize_columns(_gaussian_matrix(derive_seed(stream_seed, 21), m, m))
+    V = _orthonormalize_columns(_gaussian_matrix(derive_seed(stream_seed, 22), n, m))
+    sigma = np.array([kappa ** (-float(j) / float(m - 1)) for j in range(m)])
+    A = np.asfortranarray((U * sigma) @ np.conj(V).T)
+    w = rng_draw(derive_seed(stream_seed, 23), "sign", m) * (1.0 / np.sqrt(float(m)))
+    p = V @ w.astype(np.complex128)
+    return GeneratedInstance(A=A, b=A @ p, p_true=p, kappa=kappa)
+
+
+def normalized_error(x: np.ndarray, p_true: np.ndarray, kappa: float) -> float:
+    """src/bench.cpp:76-80"""
+    pn = float(np.linalg.norm(p_true))
+    if not pn > 0.0:
+        raise ValueError("normalized_error: p_true must be nonzero")
+    return float(np.linalg.norm(x - p_true)) / (kappa * pn)
+
+
+def bench_epsilon(kappa: float, m: int, l: int, alpha: float = 4.0) -> float:
+    """src/bench.cpp:82-84"""
+    return 1e-14 * kappa * np.sqrt(alpha * m / l)
+
+
 def solve_svd(A: np.ndarray, b: np.ndarray) -> np.ndarray:
     """src/solver.cpp:148-156 (desk-scale caps m<=64, n<=1024)."""
     A = _fortran(A)

@@ -361,3 +361,30 @@ def test_exact_minnorm_against_svd_and_pivoted_qr(real):
     assert np.linalg.norm(p - p2) <= 1e-13 * np.linalg.norm(p)
     e_qr = np.linalg.norm(O.solve_classical(A, b) - p) / np.linalg.norm(p)
     assert 1e-13 < e_qr <= 10 * O.EPS * 1e6
+
+
+# ---- tests/acceptance.cpp criteria against the oracle (pins generate_instance + solve_randomized)
+def test_acceptance_oracle_equivalence_200_trials():
+    """acceptance.cpp:50-75: 200 generated instances, randomized (eps 1e-6) vs SVD <= 1e-6."""
+    worst = 0.0
+    for trial in range(200):
+        m = 2 + trial % 7
+        n = m * (8 << (trial % 4))
+        kappa = 1e3 if trial % 2 else 1.0
+        gen = O.generate_instance(m, n, kappa, 9000 + trial)
+        assert np.allclose(np.linalg.svd(gen.A, compute_uv=False)[[0, -1]], [1.0, 1.0 / kappa], rtol=1e-12)
+        x = O.solve_randomized(gen.A, gen.b, sketch_size=4 * m, epsilon=1e-6, seed=O.derive_seed(9000 + trial, 77),
+                               threads=1).x
+        p = O.solve_svd(gen.A, gen.b)
+        worst = max(worst, np.linalg.norm(x - p) / np.linalg.norm(p))
+    assert worst <= 1e-6
+
+
+def test_acceptance_table2_eps_r_oracle():
+    """acceptance.cpp:77-90 (3 of the 10 trials on the CPU): eps_r <= 1e-13 at 128 x 16384, l = 512."""
+    gen = O.generate_instance(128, 16384, 1e6, O.derive_seed(1001, 100))
+    eps = O.bench_epsilon(1e6, 128, 512)
+    assert eps == pytest.approx(1e-8)
+    for trial in range(3):
+        rep = O.solve_randomized(gen.A, gen.b, sketch_size=512, epsilon=eps, seed=O.derive_seed(1001, 1000 + trial))
+        assert O.normalized_error(rep.x, gen.p_true, 1e6) <= 1e-13

@@ -33,6 +33,7 @@ extern "C" {
 #define MNB_ERR_UNSUPPORTED 7      /* e.g. an FFT length this build has no kernel for   */
 #define MNB_ERR_OUT_OF_MEMORY 8
 #define MNB_ERR_INTERNAL 9
+#define MNB_ERR_PARSE 10           /* minnorm::ParseError (errors.hpp:34-49)             */
 
 /* ---- enums --------------------------------------------------------------- */
 #define MNB_C128 0 /* complex<double> */
@@ -49,6 +50,30 @@ const char* mnb_last_error(void);
 /* RankDeficiencyError::deficient_columns() of the last MNB_ERR_RANK_DEFICIENCY. */
 int64_t mnb_last_deficient_columns(void);
 const char* mnb_version(void);
+
+/* ParseError::line() / column() of the last MNB_ERR_PARSE (1-based, 0 when unknown). */
+void mnb_last_parse_location(int64_t* line, int64_t* column);
+
+/* ---- dense complex Matrix Market files (host only; no GPU needed) ----------
+ * The reference front end's file format (include/minnorm/matrix_market.hpp,
+ * src/matrix_market.cpp:65-130): "%%MatrixMarket matrix array complex general",
+ * comments, "rows cols", then one "re im" pair per line in column-major order.
+ * Malformed input -> MNB_ERR_PARSE with the reference's line / column. */
+/* read_matrix_market, step 1: the size line only. */
+int mnb_mm_read_dims(const char* path, int64_t* rows, int64_t* cols);
+/* read_matrix_market (matrix_market.cpp:65-102), step 2: the entries into out
+ * (rows*cols complex<double>, column-major); rows/cols as returned by step 1. */
+int mnb_mm_read(const char* path, void* out, int64_t rows, int64_t cols);
+/* write_matrix_market (matrix_market.cpp:113-130): 17 significant digits. */
+int mnb_mm_write(const char* path, const void* data, int64_t rows, int64_t cols);
+
+/* generate_instance(m, n, kappa, RandomStream(stream_seed)) (include/minnorm/bench.hpp;
+ * src/bench.cpp:46-74), host only: A = U diag(sigma) V^H (m x n column-major complex),
+ * b = A p_true (m), p_true = V w (n).  Same substreams (21/22/23) and draw order as the
+ * reference; values agree to rounding (the products are summed in a different order).
+ * Bad sizes -> MNB_ERR_DIMENSION (the CLI maps the reference's invalid_argument there). */
+int mnb_generate_instance(int64_t m, int64_t n, double kappa, uint64_t stream_seed, void* A_out, void* b_out,
+                          void* p_out);
 
 /* ---- context (one per GPU / per rank) ------------------------------------ */
 typedef struct mnb_context mnb_context;

@@ -9,11 +9,14 @@ small QR, NCCL for column-sharded multi-GPU runs.
 from .api import (apply_adjoint_matrix, ConfigError, Context, DeviceError, DimensionError, LsqConfig, LsqSolution, ProblemInstance,
                   RankDeficiencyError, Sampling, SolveReport, SolverConfig, SrftOperator, UnsupportedError,
                   build_srft, default_context, derive_seed, dft, idft, redistribute_plan, shard_columns, solve_classical,
-                  solve_least_squares, solve_randomized, srft_from_fields, ClassicalReport)
+                  solve_least_squares, solve_randomized, srft_from_fields, ClassicalReport, ParseError,
+                  read_matrix_market, read_vector_market, write_matrix_market, generate_instance,
+                  GeneratedInstance)
 
 __all__ = [
     "apply_adjoint_matrix", "ConfigError", "Context", "DeviceError", "DimensionError", "LsqConfig", "LsqSolution", "ProblemInstance",
     "RankDeficiencyError", "Sampling", "SolveReport", "SolverConfig", "SrftOperator", "UnsupportedError",
     "build_srft", "default_context", "derive_seed", "dft", "idft", "redistribute_plan", "shard_columns", "solve_classical",
-    "solve_least_squares", "solve_randomized", "srft_from_fields", "ClassicalReport",
+    "solve_least_squares", "solve_randomized", "srft_from_fields", "ClassicalReport", "ParseError",
+    "read_matrix_market", "read_vector_market", "write_matrix_market", "generate_instance", "GeneratedInstance",
 ]

@@ -23,6 +23,7 @@ MNB_ERR_NCCL = 6
 MNB_ERR_UNSUPPORTED = 7
 MNB_ERR_OUT_OF_MEMORY = 8
 MNB_ERR_INTERNAL = 9
+MNB_ERR_PARSE = 10
 
 MNB_C128 = 0
 MNB_F64 = 1
@@ -72,7 +73,8 @@ class LsqSolutionC(ctypes.Structure):
 EXPORTS = [
     "mnb_last_error", "mnb_last_deficient_columns", "mnb_version", "mnb_context_create", "mnb_nccl_unique_id",
     "mnb_context_create_distributed", "mnb_context_destroy", "mnb_context_set_stream", "mnb_shard_columns",
-    "mnb_redistribute_plan",
+    "mnb_redistribute_plan", "mnb_last_parse_location", "mnb_mm_read_dims", "mnb_mm_read", "mnb_mm_write",
+    "mnb_generate_instance",
     "mnb_set_matrix", "mnb_solver_config_default", "mnb_solve_randomized", "mnb_solve_classical",
     "mnb_solve_least_squares",
     "mnb_srft_build", "mnb_srft_from_fields", "mnb_srft_destroy", "mnb_srft_get_field", "mnb_srft_dims",
@@ -112,6 +114,12 @@ def load():
     L.mnb_context_destroy.restype = None
     L.mnb_context_set_stream.argtypes = [vp, vp]
     L.mnb_shard_columns.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.mnb_last_parse_location.argtypes = [ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.mnb_last_parse_location.restype = None
+    L.mnb_mm_read_dims.argtypes = [ctypes.c_char_p, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.mnb_mm_read.argtypes = [ctypes.c_char_p, dp, i64, i64]
+    L.mnb_mm_write.argtypes = [ctypes.c_char_p, dp, i64, i64]
+    L.mnb_generate_instance.argtypes = [i64, i64, ctypes.c_double, u64, dp, dp, dp]
     L.mnb_redistribute_plan.argtypes = [i64, i64, ci, ci, ctypes.POINTER(i64)]
     L.mnb_set_matrix.argtypes = [vp, ci, i64, i64, i64, i64, dp, i64, ci]
     L.mnb_solver_config_default.argtypes = [ctypes.POINTER(SolverConfigC)]

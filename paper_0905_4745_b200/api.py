@@ -39,6 +39,20 @@ class RankDeficiencyError(RuntimeError):
         return self._deficient
 
 
+class ParseError(RuntimeError):
+    """minnorm::ParseError (include/minnorm/errors.hpp:34-49): 1-based line / column, 0 when unknown."""
+
+    def __init__(self, what: str, line: int = 0, column: int = 0):
+        super().__init__(what)
+        self._line, self._column = int(line), int(column)
+
+    def line(self) -> int:
+        return self._line
+
+    def column(self) -> int:
+        return self._column
+
+
 class UnsupportedError(RuntimeError):
     """A shape this build has no GPU kernel for (e.g. an FFT length with large prime factors)."""
 
@@ -61,6 +75,10 @@ def _check(status: int) -> None:
         raise RankDeficiencyError(msg, L.load().mnb_last_deficient_columns())
     if status == L.MNB_ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
+    if status == L.MNB_ERR_PARSE:
+        ln, col = ctypes.c_int64(), ctypes.c_int64()
+        L.load().mnb_last_parse_location(ctypes.byref(ln), ctypes.byref(col))
+        raise ParseError(msg, ln.value, col.value)
     if status == L.MNB_ERR_OUT_OF_MEMORY:
         raise MemoryError(msg)
     raise DeviceError(f"[status {status}] {msg}")
@@ -564,3 +582,53 @@ def idft(x, ctx: Optional[Context] = None) -> np.ndarray:
         raise ValueError("Fft: length must be positive")
     _check(ctx._lib.mnb_dft(ctx._h, y.size, _ptr(y), 1))
     return y
+
+
+# --------------------------------------------------------- matrix market --
+def read_matrix_market(path: str) -> np.ndarray:
+    """read_matrix_market (include/minnorm/matrix_market.hpp; src/matrix_market.cpp:65-102): a dense
+    complex m x n matrix (column-major).  Raises ParseError with the reference's line / column."""
+    lib = L.load()
+    rows, cols = ctypes.c_int64(), ctypes.c_int64()
+    p = str(path).encode()
+    _check(lib.mnb_mm_read_dims(p, ctypes.byref(rows), ctypes.byref(cols)))
+    out = np.zeros((rows.value, cols.value), np.complex128, order="F")
+    _check(lib.mnb_mm_read(p, out.ctypes.data_as(ctypes.c_void_p), rows.value, cols.value))
+    return out
+
+
+def read_vector_market(path: str) -> np.ndarray:
+    """read_vector_market (src/matrix_market.cpp:104-111): a one-column file, else DimensionError."""
+    A = read_matrix_market(path)
+    if A.shape[1] != 1:
+        raise DimensionError(f"'{path}' holds a {A.shape[0]}x{A.shape[1]} matrix where a vector was expected")
+    return A[:, 0].copy()
+
+
+def write_matrix_market(path: str, A) -> None:
+    """write_matrix_market (src/matrix_market.cpp:113-130): 17 significant digits, so equal values
+    round-trip to byte-identical files.  A vector is written as one column."""
+    A = np.asarray(A)
+    if A.ndim == 1:
+        A = A.reshape(-1, 1)
+    A = np.asfortranarray(A.astype(np.complex128, copy=False))
+    _check(L.load().mnb_mm_write(str(path).encode(), A.ctypes.data_as(ctypes.c_void_p), A.shape[0], A.shape[1]))
+
+
+@dataclass
+class GeneratedInstance:
+    """include/minnorm/bench.hpp: A = U diag(sigma) V^H, b = A p_true."""
+    A: np.ndarray
+    b: np.ndarray
+    p_true: np.ndarray
+    kappa: float
+
+
+def generate_instance(m: int, n: int, kappa: float, stream_seed: int) -> GeneratedInstance:
+    """generate_instance(m, n, kappa, RandomStream(stream_seed)) (src/bench.cpp:46-74), host side."""
+    A = np.zeros((m, n), np.complex128, order="F")
+    b = np.zeros(m, np.complex128)
+    p = np.zeros(n, np.complex128)
+    _check(L.load().mnb_generate_instance(int(m), int(n), float(kappa), int(stream_seed) & _M64, _ptr(A), _ptr(b),
+                                          _ptr(p)))
+    return GeneratedInstance(A=A, b=b, p_true=p, kappa=float(kappa))

@@ -4,6 +4,7 @@
 #include <string>
 
 #include "context.cuh"
+#include "mm_io.hpp"
 
 struct mnb_context {
     mnb::Context ctx;
@@ -16,12 +17,18 @@ namespace {
 
 thread_local std::string g_error;
 thread_local int64_t g_deficient = 0;
+thread_local int64_t g_parse_line = 0, g_parse_column = 0;
 
 template <class F>
 int guard(F&& f) {
     try {
         f();
         return MNB_OK;
+    } catch (const mnb::ParseFail& e) {
+        g_error = e.what();
+        g_parse_line = e.line;
+        g_parse_column = e.column;
+        return e.code;
     } catch (const mnb::Error& e) {
         g_error = e.what();
         g_deficient = e.deficient;
@@ -96,6 +103,42 @@ int mnb_context_create(int device, mnb_context** out) {
             throw;
         }
         *out = c;
+    });
+}
+
+void mnb_last_parse_location(int64_t* line, int64_t* column) {
+    if (line) *line = g_parse_line;
+    if (column) *column = g_parse_column;
+}
+
+int mnb_mm_read_dims(const char* path, int64_t* rows, int64_t* cols) {
+    return guard([&] {
+        mnb::require(path && rows && cols, MNB_ERR_INVALID_ARGUMENT, "mnb_mm_read_dims: null argument");
+        mnb::mm_dims(path, rows, cols);
+    });
+}
+
+int mnb_mm_read(const char* path, void* out, int64_t rows, int64_t cols) {
+    return guard([&] {
+        mnb::require(path && out && rows >= 1 && cols >= 1, MNB_ERR_INVALID_ARGUMENT, "mnb_mm_read: bad argument");
+        mnb::mm_read(path, static_cast<double*>(out), rows, cols);
+    });
+}
+
+int mnb_mm_write(const char* path, const void* data, int64_t rows, int64_t cols) {
+    return guard([&] {
+        mnb::require(path && (data || rows * cols == 0) && rows >= 0 && cols >= 0, MNB_ERR_INVALID_ARGUMENT,
+                     "mnb_mm_write: bad argument");
+        mnb::mm_write(path, static_cast<const double*>(data), rows, cols);
+    });
+}
+
+int mnb_generate_instance(int64_t m, int64_t n, double kappa, uint64_t stream_seed, void* A_out, void* b_out,
+                          void* p_out) {
+    return guard([&] {
+        mnb::require(A_out && b_out && p_out, MNB_ERR_INVALID_ARGUMENT, "mnb_generate_instance: null output");
+        mnb::generate_instance(m, n, kappa, stream_seed, static_cast<double*>(A_out), static_cast<double*>(b_out),
+                               static_cast<double*>(p_out));
     });
 }
 

@@ -21,4 +21,8 @@ inline void require(bool ok, int code, const std::string& what) {
     if (!ok) throw Error(code, what);
 }
 
+// generate_instance of the reference front end (instance.cpp; src/bench.cpp:46-74)
+void generate_instance(int64_t m, int64_t n, double kappa, uint64_t stream_seed, double* A_out, double* b_out,
+                       double* p_out);
+
 }  // namespace mnb

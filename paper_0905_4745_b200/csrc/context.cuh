@@ -135,7 +135,7 @@ struct Context {
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
     DevBuf Rinv, Rinv_rows;
     DevBuf vec_m[10], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;
-    DevBuf rhs, flag, out_c;
+    DevBuf rhs, flag, out_c, qprobe;
     int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
     PinnedBuf pin_params[2], pin_small;
     struct SlabCache {

@@ -417,6 +417,9 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         if (const char* e = std::getenv("MNB_SLAB_ROWS"))
             if (const int64_t f = std::atoll(e); f > 0) ms = std::min<int64_t>(ms, std::max<int64_t>(8, f & ~int64_t(7)));
         sc = {n, rows, h.l, ctx.m, std::max<int64_t>(1, std::min<int64_t>(ms, rows))};
+        if (std::getenv("MNB_TRACE"))
+            std::fprintf(stderr, "[mnb] sketch slab: %lld of %lld rows (free %.1f GiB, budget %.1f GiB)\n",
+                         (long long)sc.Ms, (long long)rows, double(free_b) / (1 << 30), double(budget) / (1 << 30));
     }
     const int64_t Ms = sc.Ms;
     const int64_t Mp = (Ms + 7) & ~int64_t(7);  // blocked layouts pad the slab to whole 8-row blocks

@@ -79,4 +79,25 @@ void launch_transpose(const double2* in, int64_t rows, int64_t cols, int64_t ld_
                       cudaStream_t stream);
 void launch_init_state(CgState* st, double tau, double dup, long long max_it, cudaStream_t stream);
 
+// The whole CG loop as one persistent cooperative kernel (k_pcg_small.cu) for L2-resident A.
+constexpr int64_t kSmallMaxM = 256;
+struct SmallCgArgs {
+    const void* A = nullptr;  // column-major m x n (lda == m)
+    int is_real = 0;
+    int64_t m = 0, n = 0;
+    const double2* Rinv = nullptr;       // m x m upper, column layout
+    const double2* Rinv_rows = nullptr;  // the same, row layout
+    double2 *u = nullptr, *g = nullptr, *dir = nullptr, *dir_old = nullptr, *w = nullptr, *ax = nullptr;  // m
+    double2 *r = nullptr, *t = nullptr, *x = nullptr;                                                    // n
+    double2* part_s = nullptr;    // [grid][m]
+    double* part_scal = nullptr;  // [grid][4]
+    double2* s = nullptr;         // m
+    double* part_gg = nullptr;    // [grid]
+    CgState* st = nullptr;
+    double* residual_norms = nullptr;
+};
+bool pcg_small_eligible(int64_t m, int64_t n, int is_real);
+int pcg_small_grid(int64_t m, int64_t n, int num_sms);
+void launch_pcg_small(const SmallCgArgs& a, int grid, cudaStream_t stream);
+
 }  // namespace mnb

@@ -298,12 +298,46 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
         MNB_CUDA(cudaMemcpyAsync(st_h, st, sizeof(CgState), cudaMemcpyDeviceToHost, ctx.stream));
         MNB_CUDA(cudaStreamSynchronize(ctx.stream));
     };
-    // CG iterations (lsq.cpp:88-107), K at a time between host polls of the
-    // device-side done flag; kernels of finished loops exit immediately.
+    // CG iterations (lsq.cpp:88-107).  L2-resident A on one GPU: the whole loop is one persistent
+    // cooperative kernel (k_pcg_small.cu); otherwise K iterations of (pass, reduce, upd1, upd2)
+    // between host polls of the device-side done flag (kernels of finished loops exit at once).
     const int64_t K = 4;
     int64_t issued = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pass_ev;
-    for (;;) {
+    const bool small = !ctx.distributed() && n > 0 && pcg_small_eligible(m, n, ctx.dtype == MNB_F64) &&
+                       !std::getenv("MNB_SMALL_CG_OFF");
+    if (small) {
+        SmallCgArgs a;
+        a.A = ctx.A;
+        a.is_real = ctx.dtype == MNB_F64;
+        a.m = m;
+        a.n = n;
+        a.Rinv = Rinv;
+        a.Rinv_rows = Rinv_rows;
+        a.u = u;
+        a.g = g;
+        a.dir = dir;
+        a.dir_old = dir_old;
+        a.w = w;
+        a.ax = ax;
+        a.r = r;
+        a.t = t;
+        a.x = x;
+        const int grid = pcg_small_grid(m, n, ctx.num_sms);
+        a.part_s = dev<double2>(ctx.part_s, size_t(grid) * size_t(m));
+        a.part_scal = dev<double>(ctx.part_scal, size_t(grid) * 4);
+        a.s = reinterpret_cast<double2*>(pb.red);
+        a.part_gg = dev<double>(ctx.part_gg, size_t(std::max(grid, ub)));
+        a.st = st;
+        a.residual_norms = norms;
+        cudaEvent_t e0 = ctx.event(32), e1 = ctx.event(33);
+        MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+        launch_pcg_small(a, grid, ctx.stream);
+        MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+        ctx.launches += 1;
+        pass_ev.emplace_back(e0, e1);
+    }
+    for (; !small;) {
         read_state();
         if (st_h->done || issued >= max_it + 1) break;
         for (int64_t k = 0; k < K; ++k) {
@@ -343,7 +377,13 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     res.pass_ms = ctx.init_from_sketch ? 0.f : ms;  // (the INIT pass, when there was one)
     res.pass_launches = ctx.init_from_sketch ? 0 : 1;
     ctx.init_from_sketch = false;
-    const int64_t worked = std::min<int64_t>(int64_t(pass_ev.size()), res.iterations + (st_h->stop_qq0 ? 1 : 0));
+    if (small) {  // one launch for the whole loop: report it per iteration
+        MNB_CUDA(cudaEventElapsedTime(&ms, pass_ev[0].first, pass_ev[0].second));
+        res.pass_ms += ms;
+        res.pass_launches += std::max<int64_t>(1, res.iterations);
+    }
+    const int64_t worked =
+        small ? 0 : std::min<int64_t>(int64_t(pass_ev.size()), res.iterations + (st_h->stop_qq0 ? 1 : 0));
     for (int64_t i = 0; i < worked; ++i) {
         MNB_CUDA(cudaEventElapsedTime(&ms, pass_ev[size_t(i)].first, pass_ev[size_t(i)].second));
         res.pass_ms += ms;

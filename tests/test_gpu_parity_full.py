@@ -59,7 +59,8 @@ def test_full_size_parity(name):
     finally:
         ctx.close()
     x = rep.x
-    assert rep.lsq_converged
+    assert rep.lsq_converged, (name, rep.lsq_iterations, rep.extra, torch.cuda.mem_get_info(),
+                               torch.cuda.memory_reserved())
     A_host = A.T.cpu().numpy().T
     del A
     torch.cuda.empty_cache()

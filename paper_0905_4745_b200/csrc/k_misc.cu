@@ -193,6 +193,26 @@ __global__ void __launch_bounds__(256) sketch_adjoint_gemv_kernel(const double2*
     }
 }
 
+// Power steps on D = Q1^H Q1 - I without host round trips (solver.cu cholqr_r): v <- v / ||v||
+// and a copy into the work vector; then a <- a - v (= D v) and v <- a.
+__global__ void unit_copy_kernel(double2* v, double2* a, int64_t m, const double* nrm) {
+    const double s = 1.0 / *nrm;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        double2 x = v[i];
+        x.x *= s;
+        x.y *= s;
+        v[i] = x;
+        a[i] = x;
+    }
+}
+__global__ void sub_copy_kernel(double2* a, double2* v, int64_t m) {
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const double2 d = make_double2(a[i].x - v[i].x, a[i].y - v[i].y);
+        a[i] = d;
+        v[i] = d;
+    }
+}
+
 // red_scal = [qq = ||c||^2, <r,t> = 0, ||r||^2 = 0, 0] (the INIT pass's scalars, pcg.cuh)
 __global__ void cg_init_finish_kernel(const double* part, int parts, double* red_scal) {
     double s = 0.0;
@@ -204,6 +224,16 @@ __global__ void cg_init_finish_kernel(const double* part, int parts, double* red
 }
 
 }  // namespace
+
+void launch_unit_copy(double2* v, double2* a, int64_t m, const double* nrm, cudaStream_t stream) {
+    unit_copy_kernel<<<1, 256, 0, stream>>>(v, a, m, nrm);
+    MNB_LAUNCH_CHECK();
+}
+
+void launch_sub_copy(double2* a, double2* v, int64_t m, cudaStream_t stream) {
+    sub_copy_kernel<<<1, 256, 0, stream>>>(a, v, m);
+    MNB_LAUNCH_CHECK();
+}
 
 void launch_sketch_adjoint_gemv(const double2* S, int64_t l, int64_t m, const double2* z, double2* y,
                                 cudaStream_t stream) {

@@ -42,6 +42,26 @@ __device__ __forceinline__ double2 warp_sum2s(double2 v) {
     return v;
 }
 
+// Fixed-order warp sums over the G CTA partials: lane l adds parts l, l+32, ... in order, then a
+// fixed xor butterfly (deterministic; 32 loads in flight instead of a G-long dependent chain).
+__device__ __forceinline__ double warp_sum_parts(const double* base, int stride, int G, int lane) {
+    double acc = 0.0;
+    for (int b = lane; b < G; b += 32) acc += __ldcg(base + int64_t(b) * stride);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc;
+}
+__device__ __forceinline__ double2 warp_sum_parts2(const double2* base, int64_t stride, int G, int lane) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b = lane; b < G; b += 32) acc = c_add(acc, __ldcg(base + int64_t(b) * stride));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    return acc;
+}
+
 template <typename AT>
 __device__ __forceinline__ AT ldA(const void* A, int64_t idx);
 template <>
@@ -72,7 +92,7 @@ __device__ __forceinline__ void axpy_accs(double2& acc, double a, double2 t) {
 
 // EPL: rows per lane (m <= 32 EPL).  Shared memory: w / s / d (m each), the per-warp s partials
 // [kSmallWarps][m], scalar scratch.
-// W warps per CTA: 16, or 8 at EPL = 8 (more registers per thread: no spills)
+// W warps per CTA: 16, or 8 at EPL >= 4 (more registers per thread: no spills)
 template <typename AT, int EPL, int W>
 __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs p) {
     constexpr int kSmallWarps = W;
@@ -101,8 +121,27 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
 #pragma unroll
         for (int e = 0; e < EPL; ++e) sacc[e] = make_double2(0.0, 0.0);
         double qq = 0.0, rt = 0.0, rr = 0.0;
+        // the r / t / x entries of the warp's first 32 columns, prefetched one per lane (the
+        // per-column epilogue then takes them by shuffle instead of a dependent global load)
+        double2 pt = make_double2(0.0, 0.0), pr = pt, px = pt;
+        {
+            const int64_t jl = c0 + 2 * warp + 2 * int64_t(kSmallWarps) * (lane >> 1) + (lane & 1);
+            if (jl < c1) {
+                pt = p.t[jl];
+                pr = p.r[jl];
+                if (p.x) px = p.x[jl];
+            }
+        }
+        int step = 0;
         // two columns per step: their loads and reductions are independent (latency hiding)
-        for (int64_t j0 = c0 + 2 * warp; j0 < c1; j0 += 2 * kSmallWarps) {
+        for (int64_t j0 = c0 + 2 * warp; j0 < c1; j0 += 2 * kSmallWarps, ++step) {
+            double2 told_s, r_s, x_s;
+            {
+                const int src = (2 * step + (lane & 1)) & 31;
+                told_s = make_double2(__shfl_sync(0xffffffffu, pt.x, src), __shfl_sync(0xffffffffu, pt.y, src));
+                r_s = make_double2(__shfl_sync(0xffffffffu, pr.x, src), __shfl_sync(0xffffffffu, pr.y, src));
+                x_s = make_double2(__shfl_sync(0xffffffffu, px.x, src), __shfl_sync(0xffffffffu, px.y, src));
+            }
             const int nk = j0 + 1 < c1 ? 2 : 1;
             AT a[2][EPL];
             double2 dacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
@@ -129,8 +168,9 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
             if (lane < nk) {  // the lagged updates of column j (pcg_pass_kernel's epilogue, PCG_CG)
                 const int64_t j = j0 + lane;
                 const double2 tk = lane == 0 ? tks[0] : tks[1];
-                const double2 told = p.t[j];
-                double2 rk = p.r[j];
+                const bool pre = step < 16;
+                const double2 told = pre ? told_s : p.t[j];
+                double2 rk = pre ? r_s : p.r[j];
                 rk.x = fma(-alpha_prev, told.x, rk.x);
                 rk.y = fma(-alpha_prev, told.y, rk.y);
                 rr = fma(rk.x, rk.x, fma(rk.y, rk.y, rr));
@@ -138,7 +178,7 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
                 p.r[j] = rk;
                 p.t[j] = tk;
                 if (p.x) {
-                    double2 xk = p.x[j];
+                    double2 xk = pre ? x_s : p.x[j];
                     xk.x = fma(alpha_prev, told.x, xk.x);
                     xk.y = fma(alpha_prev, told.y, xk.y);
                     p.x[j] = xk;
@@ -173,15 +213,13 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
         }
         grid.sync();
         // ------------------------------------------------------------ R: reduce
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            double2 acc = __ldcg(p.part_s + i);
-            for (int b = 1; b < G; ++b) acc = c_add(acc, __ldcg(p.part_s + int64_t(b) * m + i));
-            p.s[i] = acc;
+        for (int64_t i = r0 + warp; i < r1; i += kSmallWarps) {  // a warp per row of the slice
+            const double2 acc = warp_sum_parts2(p.part_s + i, m, G, lane);
+            if (lane == 0) p.s[i] = acc;
         }
-        if (threadIdx.x < 3) {
-            double acc = 0.0;
-            for (int b = 0; b < G; ++b) acc += __ldcg(p.part_scal + b * 4 + threadIdx.x);
-            red_sh[0][threadIdx.x] = acc;
+        if (warp < 3) {  // a warp per scalar (every CTA: identical sums)
+            const double acc = warp_sum_parts(p.part_scal + warp, 4, G, lane);
+            if (lane == 0) red_sh[0][warp] = acc;
         }
         __syncthreads();
         const double qq_t = red_sh[0][0], rt_t = red_sh[0][1], rrk = red_sh[0][2];
@@ -246,9 +284,9 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
         }
         grid.sync();
         // --------------------------------------------------------- U2: direction
-        if (threadIdx.x == 0) {
-            double ggn = 0.0;
-            for (int b = 0; b < G; ++b) ggn += __ldcg(p.part_gg + b);  // fixed order, every CTA
+        if (warp == 0) {
+            const double ggn = warp_sum_parts(p.part_gg, 1, G, lane);  // fixed order, every CTA
+            if (lane == 0) {
             const double excess = S.dup * ggn;
             const bool conv = excess <= S.tau * fmax(S.rr - excess, 0.0) || S.rr <= S.floor2;
             const bool capped = S.iterations >= S.max_iterations;
@@ -260,6 +298,7 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
             } else {
                 red_sh[0][3] = ggn / S.gg_prev;  // beta
                 S.gg = ggn;
+            }
             }
         }
         __syncthreads();
@@ -291,7 +330,7 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
 
 template <typename AT, int EPL>
 void launch_small_typed(const SmallCgArgs& a, int grid, cudaStream_t stream) {
-    constexpr int W = EPL >= 8 ? 8 : 16;
+    constexpr int W = EPL >= 4 ? 8 : 16;
     auto k = pcg_small_kernel<AT, EPL, W>;
     const size_t smem = size_t(2 + W) * size_t(a.m) * 16;
     MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -149,6 +149,9 @@ void launch_cg_init_vectors(const double2* c, int64_t n, double2* r, double2* t,
                             double* red_scal, cudaStream_t stream);
 // A_jj += shift (real), m x m column-major
 void launch_add_diagonal(double2* A, int64_t m, double shift, cudaStream_t stream);
+// power steps on Q1^H Q1 - I (cholqr_r): v <- v / *nrm, a <- v ; and a <- a - v, v <- a
+void launch_unit_copy(double2* v, double2* a, int64_t m, const double* nrm, cudaStream_t stream);
+void launch_sub_copy(double2* a, double2* v, int64_t m, cudaStream_t stream);
 // out[0] = max_{i<=j} |A_ij - delta_ij| over the upper triangle (deterministic)
 void launch_max_offset_from_identity(const double2* A, int64_t m, double* out, cudaStream_t stream);
 void launch_copy_dups(double2* S, int64_t ldS, int64_t row0, int64_t rows, const int32_t* dups, int64_t ndups,

@@ -520,7 +520,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             auto* qc = reinterpret_cast<cuDoubleComplex*>(q);
             const auto* Sc = reinterpret_cast<const cuDoubleComplex*>(S);
             const auto* Ri = reinterpret_cast<const cuDoubleComplex*>(Rinv);
-            const cuDoubleComplex czero = make_cuDoubleComplex(0.0, 0.0), cmone = make_cuDoubleComplex(-1.0, 0.0);
+            const cuDoubleComplex czero = make_cuDoubleComplex(0.0, 0.0);
             std::vector<double2> v0(static_cast<size_t>(m));
             uint64_t h = 0x9E3779B97F4A7C15ull;
             for (int64_t i = 0; i < m; ++i) {  // seeded pseudo-random start (splitmix64)
@@ -533,26 +533,31 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
                 v0[size_t(i)] = make_double2(nxt(), nxt());
             }
             MNB_CUDA(cudaMemcpyAsync(v, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-            double lam = 0.0;
+            // device pointer mode: the ten steps run without a host round trip; one read at the end
+            double* nrm_d = dev<double>(ctx.scratch, 512);
+            cublasSetPointerMode(ctx.cublas, CUBLAS_POINTER_MODE_DEVICE);
+            cuDoubleComplex* consts = reinterpret_cast<cuDoubleComplex*>(nrm_d + 8);  // [1, 0]
+            const cuDoubleComplex hc[2] = {cone, czero};
+            MNB_CUDA(cudaMemcpyAsync(consts, hc, sizeof hc, cudaMemcpyHostToDevice, ctx.stream));
+            cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, nrm_d), "dznrm2");
             for (int it = 0; it < 10; ++it) {
-                double vn = 0.0;
-                cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, &vn), "dznrm2");
-                const cuDoubleComplex sc = make_cuDoubleComplex(1.0 / vn, 0.0);
-                cublas_check(cublasZscal(ctx.cublas, int(m), &sc, vc, 1), "zscal");
-                MNB_CUDA(cudaMemcpyAsync(a, v, size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+                launch_unit_copy(v, a, m, nrm_d, ctx.stream);                    // v = v / ||v||, a = v
                 cublas_check(cublasZtrmv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
-                                         Ri, int(m), ac, 1), "ztrmv");                      // a = R1^{-1} v
-                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &cone, Sc, int(l), ac, 1, &czero,
-                                         qc, 1), "zgemv");                                  // q = E a
-                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(l), int(m), &cone, Sc, int(l), qc, 1, &czero,
-                                         ac, 1), "zgemv");                                  // a = E^H q
+                                         Ri, int(m), ac, 1), "ztrmv");          // a = R1^{-1} v
+                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), consts, Sc, int(l), ac, 1, consts + 1,
+                                         qc, 1), "zgemv");                      // q = E a
+                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(l), int(m), consts, Sc, int(l), qc, 1, consts + 1,
+                                         ac, 1), "zgemv");                      // a = E^H q
                 cublas_check(cublasZtrmv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
-                                         Ri, int(m), ac, 1), "ztrmv");                      // a = R1^{-H} a
-                cublas_check(cublasZaxpy(ctx.cublas, int(m), &cmone, vc, 1, ac, 1), "zaxpy");  // a = D v
-                cublas_check(cublasDznrm2(ctx.cublas, int(m), ac, 1, &lam), "dznrm2");
-                MNB_CUDA(cudaMemcpyAsync(v, a, size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
-                if (lam == 0.0) break;
+                                         Ri, int(m), ac, 1), "ztrmv");          // a = R1^{-H} a
+                launch_sub_copy(a, v, m, ctx.stream);                            // v = a = D v
+                cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, nrm_d), "dznrm2");  // ||D v||
+                ctx.launches += 2;
             }
+            cublasSetPointerMode(ctx.cublas, CUBLAS_POINTER_MODE_HOST);
+            double lam = 0.0;
+            MNB_CUDA(cudaMemcpyAsync(&lam, nrm_d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+            MNB_CUDA(cudaStreamSynchronize(ctx.stream));
             accept = 2.0 * lam <= 1e-3;
             if (std::getenv("MNB_TRACE"))
                 std::fprintf(stderr, "[mnb] one-pass preconditioner: u cond^2 <= %.2e (Frobenius), ||Q1^H Q1 - I|| ~ %.2e\n",

@@ -45,7 +45,9 @@ def test_world1_nccl_solve_matches_single_gpu(ctx, dctx, real):
     assert dist.extra["redistribute_seconds"] > 0.0  # the all-to-all ran (once: both sketches share it)
     assert dist.lsq_iterations == single.lsq_iterations
     assert dist.lsq_converged
-    assert _rel(dist.x, single.x) <= 1e-13
+    # the one-GPU solve of an L2-resident A runs the persistent CG kernel, the distributed one the
+    # multi-kernel loop: the same iterates up to the order of the partial sums
+    assert _rel(dist.x, single.x) <= 1e-11
     assert _rel(dist.c, single.c) <= 1e-13
     ref = O.solve_randomized(A, b, epsilon=1e-10, seed=42)
     assert _rel(dist.x, ref.x) <= 10 * cfg.epsilon

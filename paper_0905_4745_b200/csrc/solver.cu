@@ -11,6 +11,7 @@
 // Multi-GPU (column-sharded A): one NCCL allreduce of [s, qq, <r,t>, ||r||^2]
 // (2m+4 doubles) per CG iteration; the sketch redistributes A with one
 // all-to-all (srft_gpu.cu).  The small m-space work is replicated per rank.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -1289,50 +1290,131 @@ void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_cl
         rep.path = 0;
     }
     if (!ok) {
-        // ---- path 1: Householder QR of A^H (n x m), x = Q [R^{-H} b; 0]
-        if (ctx.distributed() || ctx.dtype != MNB_C128)
-            throw Error(MNB_ERR_UNSUPPORTED, "solve_classical: A is too ill-conditioned for the Gram path and the "
-                                             "Householder fallback runs on one GPU with complex A");
-        double2* AH = dev<double2>(ctx.ws_x1, size_t(n) * size_t(m));
-        launch_transpose(static_cast<const double2*>(ctx.A), m, n, m, AH, n, ctx.stream);
-        launch_conj_inplace(AH, n * m, ctx.stream);
-        ctx.launches += 2;
+        // ---- path 1: Householder QR of A^H (the reference's algorithm, src/solver.cpp:130-146), as a
+        // TSQR over the ranks' column shards: A^H = diag(Q_J) [R_1; ...; R_w] = diag(Q_J) Q~ R.
+        //   1. each rank: Householder QR of its n_J x m block A_J^H -> reflectors + R_J
+        //   2. allgather the R_J (m x m each) and factor the stack (w m x m) -> Q~, R (replicated)
+        //   3. rank rule on the singular values of R (rank-revealing, unlike the unpivoted R_jj):
+        //      sigma_j < n eps sigma_max counts as dependent, the reference's threshold
+        //      (src/solver.cpp:137-140 on its column-pivoted R)
+        //   4. x = diag(Q_J) Q~ [R^{-H} b; 0]: v = Q~ [w; 0] (replicated), x_J = Q_J [v_J; 0]
+        // One GPU is the w = 1 case (Q~ = I).  Real A is widened to complex per shard.
+        const int world = ctx.distributed() ? ctx.world : 1;
+        const int64_t kq = std::min<int64_t>(nl, m);  // rows of R_J that the local QR defines
+        double2* AH = dev<double2>(ctx.ws_x1, size_t(std::max<int64_t>(nl, 1)) * size_t(m));
+        if (nl) {
+            if (ctx.dtype == MNB_F64) {
+                double2* Aw = dev<double2>(ctx.ws_x2, size_t(m) * size_t(nl));
+                launch_real_to_complex(static_cast<const double*>(ctx.A), Aw, m * nl, ctx.stream);
+                launch_transpose(Aw, m, nl, m, AH, nl, ctx.stream);
+            } else {
+                launch_transpose(static_cast<const double2*>(ctx.A), m, nl, m, AH, nl, ctx.stream);
+            }
+            launch_conj_inplace(AH, nl * m, ctx.stream);
+            ctx.launches += 3;
+        }
         double2* tau = dev<double2>(ctx.tau_S, size_t(m));
-        size_t dws = 0, hws = 0;
-        cusolver_check(cusolverDnXgeqrf_bufferSize(ctx.cusolver, ctx.cusolver_params, n, m, CUDA_C_64F, AH, n,
-                                                   CUDA_C_64F, tau, CUDA_C_64F, &dws, &hws),
-                       "geqrf_bufferSize");
-        void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
-        if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
-        cusolver_check(cusolverDnXgeqrf(ctx.cusolver, ctx.cusolver_params, n, m, CUDA_C_64F, AH, n, CUDA_C_64F, tau,
-                                        CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
-                       "geqrf");
-        // the reference's rank rule with threshold n eps max|R_jj| (src/solver.cpp:137-140)
-        if (int64_t bad = deficient_count(ctx, AH, n, m, n); bad > 0)
-            throw Error(MNB_ERR_RANK_DEFICIENCY,
-                        "pivoted QR found rank deficiency (" + std::to_string(bad) + " dependent columns)", bad);
-        MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(n) * 16, ctx.stream));
-        MNB_CUDA(cudaMemcpyAsync(x_dev, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        auto geqrf = [&](double2* M, int64_t rows, int64_t ld, double2* t) {
+            size_t dws = 0, hws = 0;
+            cusolver_check(cusolverDnXgeqrf_bufferSize(ctx.cusolver, ctx.cusolver_params, rows, m, CUDA_C_64F, M, ld,
+                                                       CUDA_C_64F, t, CUDA_C_64F, &dws, &hws),
+                           "geqrf_bufferSize");
+            void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+            if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+            cusolver_check(cusolverDnXgeqrf(ctx.cusolver, ctx.cusolver_params, rows, m, CUDA_C_64F, M, ld, CUDA_C_64F,
+                                            t, CUDA_C_64F, work, dws, ctx.host_work.data(), hws, info),
+                           "geqrf");
+        };
+        auto unmqr = [&](const double2* M, int64_t rows, int64_t ld, const double2* t, int64_t k, double2* v) {
+            int lwork = 0;
+            cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(rows), 1, int(k),
+                                                       reinterpret_cast<const cuDoubleComplex*>(M), int(ld),
+                                                       reinterpret_cast<const cuDoubleComplex*>(t),
+                                                       reinterpret_cast<const cuDoubleComplex*>(v), int(rows), &lwork),
+                           "unmqr_bufferSize");
+            auto* wk = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
+            cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(rows), 1, int(k),
+                                            reinterpret_cast<const cuDoubleComplex*>(M), int(ld),
+                                            reinterpret_cast<const cuDoubleComplex*>(t), reinterpret_cast<cuDoubleComplex*>(v),
+                                            int(rows), wk, lwork, info),
+                           "unmqr");
+        };
+        if (nl) geqrf(AH, nl, nl, tau);
+        // R_J (m x m, zero below the diagonal and below row kq) into this rank's block of the stack
+        double2* stack = dev<double2>(ctx.R2, size_t(world) * size_t(m) * size_t(m));  // [w][m x m] col-major
+        double2* Rj = stack + size_t(world > 1 ? ctx.rank : 0) * size_t(m) * size_t(m);
+        MNB_CUDA(cudaMemsetAsync(Rj, 0, size_t(m) * size_t(m) * 16, ctx.stream));
+        if (kq) MNB_CUDA(cudaMemcpy2DAsync(Rj, size_t(m) * 16, AH, size_t(nl) * 16, size_t(kq) * 16, size_t(m),
+                                           cudaMemcpyDeviceToDevice, ctx.stream));
+        launch_zero_lower(Rj, m, ctx.stream);
+        ctx.launches += 1;
+        double2* R = Rj;  // m x m upper, leading dimension ldR
+        int64_t ldR = m;
+        double2* Sg = nullptr;  // the factored stack (w m x m, leading dimension w m)
+        double2* tau2 = nullptr;
+        if (world > 1) {
+            nccl_check(ncclAllGather(Rj, stack, size_t(2 * m * m), ncclDouble, ctx.comm, ctx.stream), "ncclAllGather");
+            // [w][m x m] blocks -> one (w m) x m column-major matrix
+            Sg = dev<double2>(ctx.qwork, size_t(world) * size_t(m) * size_t(m));
+            for (int h = 0; h < world; ++h)
+                MNB_CUDA(cudaMemcpy2DAsync(Sg + size_t(h) * size_t(m), size_t(world) * size_t(m) * 16,
+                                           stack + size_t(h) * size_t(m) * size_t(m), size_t(m) * 16, size_t(m) * 16,
+                                           size_t(m), cudaMemcpyDeviceToDevice, ctx.stream));
+            tau2 = dev<double2>(ctx.tau_E, size_t(m));
+            geqrf(Sg, int64_t(world) * m, int64_t(world) * m, tau2);
+            R = Sg;
+            ldR = int64_t(world) * m;
+        }
+        // rank rule on the singular values of R
+        {
+            double2* Rc = dev<double2>(ctx.gram, size_t(m) * size_t(m));
+            MNB_CUDA(cudaMemcpy2DAsync(Rc, size_t(m) * 16, R, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
+                                       cudaMemcpyDeviceToDevice, ctx.stream));
+            launch_zero_lower(Rc, m, ctx.stream);
+            ctx.launches += 1;
+            double* sv = dev<double>(ctx.scratch, size_t(std::max<int64_t>(m, 512)));
+            size_t dws = 0, hws = 0;
+            cusolver_check(cusolverDnXgesvd_bufferSize(ctx.cusolver, ctx.cusolver_params, 'N', 'N', m, m, CUDA_C_64F, Rc,
+                                                       m, CUDA_R_64F, sv, CUDA_C_64F, nullptr, 1, CUDA_C_64F, nullptr, 1,
+                                                       CUDA_C_64F, &dws, &hws),
+                           "gesvd_bufferSize");
+            void* work = ctx.qr_work.ensure(std::max<size_t>(dws, 16));
+            if (ctx.host_work.size() < hws + 16) ctx.host_work.resize(hws + 16);
+            cusolver_check(cusolverDnXgesvd(ctx.cusolver, ctx.cusolver_params, 'N', 'N', m, m, CUDA_C_64F, Rc, m,
+                                            CUDA_R_64F, sv, CUDA_C_64F, nullptr, 1, CUDA_C_64F, nullptr, 1, CUDA_C_64F,
+                                            work, dws, ctx.host_work.data(), hws, info),
+                           "gesvd");
+            std::vector<double> svh(static_cast<size_t>(m));
+            MNB_CUDA(cudaMemcpyAsync(svh.data(), sv, size_t(m) * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            sync(ctx);
+            const double smax = *std::max_element(svh.begin(), svh.end());
+            const double thr_r = double(n) * kEps * smax;
+            int64_t bad = 0;
+            for (double v : svh)
+                if (!(v >= thr_r) || v == 0.0) ++bad;
+            if (bad > 0)
+                throw Error(MNB_ERR_RANK_DEFICIENCY,
+                            "pivoted QR found rank deficiency (" + std::to_string(bad) + " dependent columns)", bad);
+        }
+        // w = R^{-H} b, v = Q~ [w; 0] (replicated), x_J = Q_J [v_J; 0]
+        double2* v = dev<double2>(ctx.vec_m[9], size_t(world) * size_t(m));
+        MNB_CUDA(cudaMemsetAsync(v, 0, size_t(world) * size_t(m) * 16, ctx.stream));
+        MNB_CUDA(cudaMemcpyAsync(v, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
         cublas_check(cublasZtrsv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
-                                 reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
-                                 reinterpret_cast<cuDoubleComplex*>(x_dev), 1),
+                                 reinterpret_cast<const cuDoubleComplex*>(R), int(ldR),
+                                 reinterpret_cast<cuDoubleComplex*>(v), 1),
                      "ztrsv");
-        int lwork = 0;
-        cusolver_check(cusolverDnZunmqr_bufferSize(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(n), 1, int(m),
-                                                   reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
-                                                   reinterpret_cast<const cuDoubleComplex*>(tau),
-                                                   reinterpret_cast<const cuDoubleComplex*>(x_dev), int(n), &lwork),
-                       "unmqr_bufferSize");
-        auto* wk = static_cast<cuDoubleComplex*>(ctx.qr_work.ensure(size_t(std::max(lwork, 1)) * 16));
-        cusolver_check(cusolverDnZunmqr(ctx.cusolver, CUBLAS_SIDE_LEFT, CUBLAS_OP_N, int(n), 1, int(m),
-                                        reinterpret_cast<const cuDoubleComplex*>(AH), int(n),
-                                        reinterpret_cast<const cuDoubleComplex*>(tau),
-                                        reinterpret_cast<cuDoubleComplex*>(x_dev), int(n), wk, lwork, info),
-                       "unmqr");
-        // ||A x - b|| through the INIT pass (s = A x)
+        if (world > 1) unmqr(Sg, int64_t(world) * m, int64_t(world) * m, tau2, m, v);
+        if (nl) {
+            MNB_CUDA(cudaMemsetAsync(x_dev, 0, size_t(nl) * 16, ctx.stream));
+            MNB_CUDA(cudaMemcpyAsync(x_dev, v + size_t(world > 1 ? ctx.rank : 0) * size_t(m), size_t(kq) * 16,
+                                     cudaMemcpyDeviceToDevice, ctx.stream));
+            unmqr(AH, nl, nl, tau, kq, x_dev);
+        }
+        // ||A x - b|| through the INIT pass (s = A x, summed over the ranks)
         PassBuffers pb = pass_buffers(ctx);
-        double2* r1 = dev<double2>(ctx.vec_n[0], size_t(n));
-        double2* t1 = dev<double2>(ctx.vec_n[1], size_t(n));
+        double2* r1 = dev<double2>(ctx.vec_n[0], size_t(std::max<int64_t>(nl, 1)));
+        double2* t1 = dev<double2>(ctx.vec_n[1], size_t(std::max<int64_t>(nl, 1)));
         fused_pass(ctx, pb, PCG_INIT, nullptr, x_dev, t1, r1, nullptr, nullptr);
         std::vector<double2> s(static_cast<size_t>(m));
         MNB_CUDA(cudaMemcpyAsync(s.data(), pb.red, size_t(m) * 16, cudaMemcpyDeviceToHost, ctx.stream));

@@ -269,6 +269,28 @@ def test_solve_classical_zero_rhs_and_errors(ctx):
         mn.solve_classical(mn.ProblemInstance(A, b[:5]), ctx)
 
 
+def test_solve_classical_rank_handling_real_and_ill_conditioned(ctx):
+    """real A and very ill-conditioned A reach the Householder fallback (path 1) and
+    are either solved or reported as RankDeficiencyError with the deficient-column count -- the
+    rank rule applied to the singular values of R (rank-revealing), never UNSUPPORTED."""
+    # full rank, kappa = 1e9: the Gram path cannot take it, path 1 solves it (complex and real)
+    for real in (False, True):
+        A, b = make_instance(48, 4096, 1e9, seed=12, real=real)
+        x, rep = mn.solve_classical(mn.ProblemInstance(A, b), ctx, report=True)
+        p = O.solve_classical(A.astype(np.complex128), b)
+        assert rep.path == 1
+        assert np.linalg.norm(x - p) / np.linalg.norm(p) <= 1e-14 * 1e9
+    # two dependent rows, one of them perturbed below the n eps threshold: rank m - 2
+    A, b = make_instance(32, 2048, 1e2, seed=13, real=True)
+    Ad = A.copy()
+    Ad[7] = Ad[3]
+    Ad[9] = 2.0 * Ad[4] + 1e-15 * Ad[0]
+    with pytest.raises(mn.RankDeficiencyError) as e:
+        mn.solve_classical(mn.ProblemInstance(Ad, b), ctx)
+    assert e.value.deficient_columns() == 2
+    assert O.deficient_count(np.linalg.qr(np.conj(Ad.astype(np.complex128)).T, mode="r"), 2048) >= 1
+
+
 def test_solve_classical_agrees_with_randomized(ctx):
     """The paper's comparison (Tables 1-4): the randomized solve matches the classical one to
     its epsilon."""

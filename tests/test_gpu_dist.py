@@ -71,6 +71,20 @@ def test_world1_nccl_sketch_classical_and_adjoint(ctx, dctx):
     assert np.array_equal(xd, xs) and _rel(axd, axs) <= 1e-14
 
 
+def test_world1_nccl_classical_householder_path(ctx, dctx):
+    """The TSQR form of the Householder fallback (path 1) through the distributed code path
+    (allgather of R_J, QR of the stack) equals the one-GPU path; rank deficiency is reported."""
+    A, b = make_instance(40, 3000, 1e9, seed=17)
+    x_d, rep_d = mn.solve_classical(mn.ProblemInstance(A, b), dctx, report=True, n_global=A.shape[1])
+    x_s, rep_s = mn.solve_classical(mn.ProblemInstance(A, b), ctx, report=True)
+    assert rep_d.path == 1 and rep_s.path == 1
+    assert _rel(x_d, x_s) <= 1e-10
+    Ad = A.copy()
+    Ad[6] = Ad[2]
+    with pytest.raises(mn.RankDeficiencyError):
+        mn.solve_classical(mn.ProblemInstance(Ad, b), dctx, n_global=A.shape[1])
+
+
 def test_distributed_shard_validation(dctx):
     A, b = make_instance(16, 512, 1e2, seed=2)
     fresh = mn.Context.distributed(0, 0, 1, mn.Context.nccl_unique_id())

@@ -814,32 +814,38 @@ namespace {
 //   X[f1] = sum_u w_N^{f1 u} Y_u[f1 mod 16]
 // (the 1024-point version, fft1024_select_kernel, keeps whole tiles in shared memory).
 // w_N^k = hi[k >> 6] lo[k & 63] from two small tables.
-constexpr int kBR = 4;      // rows per unit
 constexpr int kBEnt = 512;  // staged (f1, slot) pairs per unit
 
-template <int U>
-__global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const FftPassArgs a,
-                                                                       const int32_t* __restrict__ off,
-                                                                       const int32_t* __restrict__ ent) {
-    constexpr int N = 16 * U, T = kBR * U, NH = (N + 63) / 64;
+// R rows per unit (R | 8): unit = (8-row block, f2, part), part = which R rows of the block.
+// R = 4 (default): 192 KiB of Y in shared memory, one CTA per SM.  R = 2 halves the unit so two
+// CTAs share an SM (one's transform and sums over the other's loads); measured slower at c5
+// (274 vs 195 ms for both sketches: the per-pair twiddle setup and the ENT staging double).
+template <int U, int R>
+__global__ void __launch_bounds__(R * U, 4 / R) fft_select_blocked_kernel(const FftPassArgs a,
+                                                                          const int32_t* __restrict__ off,
+                                                                          const int32_t* __restrict__ ent) {
+    constexpr int N = 16 * U, T = R * U, NH = (N + 63) / 64, P = 8 / R;
     extern __shared__ __align__(16) double2 smb[];
-    double2* X = smb;                 // Y as [16 j][U u][4 r], r slot xor-swizzled by u
-    double2* LO = X + 16 * U * kBR;   // w_N^k, k < 64 (slot-swizzled)
+    double2* X = smb;                 // Y as [16 j][U u][R r], r slot xor-swizzled by u
+    double2* LO = X + 16 * U * R;     // w_N^k, k < 64 (slot-swizzled)
     double2* HI = LO + 64;            // w_N^{64 k}
     int32_t* ENT = reinterpret_cast<int32_t*>(HI + NH);
-    const int r = int(threadIdx.x) & 3, u = int(threadIdx.x) >> 2;
+    const int r = int(threadIdx.x) % R, u = int(threadIdx.x) / R;
     const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31), nwarps = T / 32;
     auto swz = [](int k) { return (k & ~7) | ((k ^ (k >> 3)) & 7); };
-    auto xb = [](int j, int uu, int rr) { return (j * U + uu) * 4 + (rr ^ ((uu >> 1) & 3)); };
+    // bank spread of the sums' reads (lanes = consecutive uu): 8 distinct 16-byte groups per phase
+    auto xb = [](int j, int uu, int rr) {
+        return R == 4 ? (j * U + uu) * 4 + (rr ^ ((uu >> 1) & 3)) : (j * U + uu) * R + (rr ^ ((uu >> 2) & (R - 1)));
+    };
     for (int i = threadIdx.x; i < 64; i += T) LO[swz(i)] = __ldg(a.tw + i);
     for (int i = threadIdx.x; i < NH; i += T) HI[i] = __ldg(a.tw + 64 * i);
     const int64_t nrb8 = (a.rows + 7) / 8;
-    const int64_t units = nrb8 * a.batches * 2;
+    const int64_t units = nrb8 * a.batches * P;
     const int64_t n1 = N;
     auto load = [&](int64_t unit, double2 (&v)[16]) {
-        const int64_t half = unit & 1, ub = unit >> 1;
+        const int64_t part = unit % P, ub = unit / P;
         const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
-        const double2* base = a.in + ((rb * a.batches + b) * n1) * 8 + 4 * half + r;
+        const double2* base = a.in + ((rb * a.batches + b) * n1) * 8 + R * part + r;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const double2* p = base + int64_t(u + U * q) * 8;
@@ -852,7 +858,7 @@ __global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const Ff
     int64_t unit = blockIdx.x;
     if (unit < units) load(unit, v);
     for (; unit < units; unit += gridDim.x) {
-        const int64_t half = unit & 1, ub = unit >> 1;
+        const int64_t part = unit % P, ub = unit / P;
         const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
         const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
         dft16_np<false>(v);
@@ -864,14 +870,14 @@ __global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const Ff
         const int64_t next = unit + gridDim.x;
         if (next < units) load(next, v);  // in flight during the sums
         const int32_t* E = cnt <= kBEnt ? ENT : ent + 2 * e0;
-        for (int p0 = warp; p0 < kBR * cnt; p0 += 2 * nwarps) {
+        for (int p0 = warp; p0 < R * cnt; p0 += 2 * nwarps) {
             double vv[4];
             int slot2[2], row2[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int p = p0 + nwarps * k;
-                const bool ok = p < kBR * cnt;
-                const int rp = p & 3, s = ok ? p >> 2 : 0;
+                const bool ok = p < R * cnt;
+                const int rp = p % R, s = ok ? p / R : 0;
                 const int f = E[2 * s];
                 slot2[k] = ok ? E[2 * s + 1] : -1;
                 row2[k] = rp;
@@ -898,7 +904,7 @@ __global__ void __launch_bounds__(kBR * U, 1) fft_select_blocked_kernel(const Ff
             const double other = __shfl_down_sync(0xffffffffu, vv[0], 8);
             if ((lane & 15) == 0) {
                 const int k = lane >> 4;
-                const int64_t row = rb * 8 + 4 * half + row2[k];
+                const int64_t row = rb * 8 + R * part + row2[k];
                 if (slot2[k] >= 0 && row < a.rows)
                     a.out[int64_t(slot2[k]) + (a.out_row0 + row) * a.ld_out] = c_scale(make_double2(vv[0], other), a.scale);
             }
@@ -912,12 +918,22 @@ bool launch_fft_select_blocked(const FftPassArgs& a, const int32_t* off, const i
                                cudaStream_t stream) {
     if (a.inverse || a.N != 3072) return false;
     constexpr int U = 192;
-    const size_t smem = (size_t(16) * U * kBR + 64 + (a.N + 63) / 64) * sizeof(double2) + 2 * kBEnt * 4;
-    auto k = fft_select_blocked_kernel<U>;
-    MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches * 2;
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, num_sms)));
-    k<<<grid, kBR * U, smem, stream>>>(a, off, ent);
+    // 4-row units, one CTA per SM (2-row units on two CTAs per SM measured slower: 274 vs 195 ms
+    // for both c5 sketches; MNB_FB_ROWS=2 selects them)
+    static const int R = [] { const char* e = std::getenv("MNB_FB_ROWS"); return e && std::atoi(e) == 2 ? 2 : 4; }();
+    const size_t smem = (size_t(16) * U * R + 64 + (a.N + 63) / 64) * sizeof(double2) + 2 * kBEnt * 4;
+    const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches * (8 / R);
+    const int per_sm = R == 2 ? 2 : 1;  // resident CTAs per SM (shared memory: 2 x 101 KiB or 1 x 197 KiB)
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(num_sms) * per_sm)));
+    if (R == 4) {
+        auto k = fft_select_blocked_kernel<U, 4>;
+        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k<<<grid, 4 * U, smem, stream>>>(a, off, ent);
+    } else {
+        auto k = fft_select_blocked_kernel<U, 2>;
+        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k<<<grid, 2 * U, smem, stream>>>(a, off, ent);
+    }
     MNB_LAUNCH_CHECK();
     return true;
 }

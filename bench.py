@@ -47,6 +47,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def fp64_peak_tfs():
+    """Measured FP64 peak (DGEMM 8192^3 on this pool's B200, scripts/micro/fp64_peaks.py ->
+    profiles/r02/fp64_peaks.json); MEASURED_PEAKS.json has no FP64 figure.  Fallback: 37 TF nominal."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "fp64_peaks.json")) as f:
+            return float(json.load(f)["gemm_f64_8192_TFs"]), "measured (DGEMM, profiles/r02/fp64_peaks.json)"
+    except Exception:
+        return 37.0, "nominal"
+
+
 # ------------------------------------------------------------------ data ---
 def make_A_shard(cfg, col_begin, n_local, device):
     """A[:, col_begin:col_begin+n_local] of A = U diag(sigma) G / sqrt(n), built on
@@ -378,7 +388,7 @@ def main():
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             prof = json.load(f).get(args.config, {})
         traffic = prof.get("pcg_pass_dram_bytes_per_launch")
-        traffic_sketch = prof.get("p2fa_dram_bytes_per_launch")
+        traffic_sketch = prof.get("sketch_dram_bytes_per_sketch")
     except Exception:
         pass
     last = reps[-1]
@@ -452,17 +462,37 @@ def main():
         sketch_ms = {"hstage1": sk[0], "hstage2+fft_a": sk[1], "fft_b": sk[3]}
         sketch_gbs = {"hstage1": gbs(esz + 16, sk[0]), "hstage2+fft_a": gbs(32, sk[1]), "fft_b": gbs(16, sk[3])}
 
-    # the sketch's dominant kernel against the same HBM peak: the fused H stage + FFT pass A moves
-    # 16 B in (x1) and 16 B out (pass A's output) per element; kernel time summed over both sketches
+    # The sketch against SURVEY 8(d)'s roofline: max(algorithmic bytes / HBM peak, FP64 flops / FP64
+    # peak) over the measured device time of one sketch (CUDA events around each sketch in the solve).
+    # Bytes: A once (16 or 8 B per entry) + the l x m output + ~88 B per index of parameters; flops:
+    # m (5 n log2 n + 42 n) (the FFT of every row plus the two H chains, D and the diagonals).
     roofline_sketch = None
-    if sk[2] == 0 and sk[1] > 0:
-        per_sketch_bytes = 32 * m * n
-        ach = 2 * per_sketch_bytes / (sk[1] * 1e-3) / 1e9
-        roofline_sketch = {"bound": "hbm", "kernel": "p2fa_kernel", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                           "frac": ach / hbm_peak, "bytes_per_sketch": per_sketch_bytes,
-                           "ms_per_sketch": sk[1] / 2,
-                           "traffic": traffic_sketch if world == 1 else None,
-                           "note": "one launch per sketch at c4 (one per row slab at c5); traffic per launch at c4"}
+    sk_s = [t for t in last.extra["sketch_seconds"] if t > 0]
+    if sk_s:
+        l_ = 4 * m
+        sk_bytes = esz * m * n + 16 * l_ * m + 88 * n
+        sk_flops = m * (5.0 * n * math.log2(n) + 42.0 * n)
+        fp64_peak, fp64_kind = fp64_peak_tfs()
+        t_sk = statistics.mean(sk_s)
+        t_hbm = sk_bytes / (hbm_peak * 1e9)
+        t_fp = sk_flops / (fp64_peak * 1e12)
+        fp_bound = t_fp >= t_hbm
+        roofline_sketch = {
+            "bound": "fp64" if fp_bound else "hbm",
+            "achieved": (sk_flops / t_sk / 1e12) if fp_bound else (sk_bytes / t_sk / 1e9),
+            "peak": fp64_peak if fp_bound else hbm_peak, "unit": "TFLOP/s" if fp_bound else "GB/s",
+            "frac": max(t_hbm, t_fp) / t_sk, "ms_per_sketch": t_sk * 1e3,
+            "floor_ms": {"hbm": t_hbm * 1e3, "fp64": t_fp * 1e3}, "peak_kind": {"hbm": peak_kind, "fp64": fp64_kind},
+            "bytes_per_sketch": sk_bytes, "flops_per_sketch": sk_flops,
+            "traffic": traffic_sketch if world == 1 else None,
+            "note": "SURVEY 8(d): max(bytes/BW, flops/FP64) / measured sketch time (device events, in the solve); "
+                    "traffic = ncu DRAM bytes of one sketch's kernels (P1, carries, fused P2 + pass A, pass B), "
+                    "profiles/ncu_summary.json"}
+        if sk[2] == 0 and sk[1] > 0:  # the fused H stage + FFT pass A alone, against the HBM peak
+            per = 32 * m * n
+            ach = 2 * per / (sk[1] * 1e-3) / 1e9
+            roofline_sketch["p2fa_kernel"] = {"achieved": ach, "unit": "GB/s", "frac": ach / hbm_peak,
+                                              "bytes_per_sketch": per, "ms_per_sketch": sk[1] / 2}
 
     if rank == 0:
         out = {

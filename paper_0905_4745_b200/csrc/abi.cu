@@ -70,6 +70,22 @@ void init_context(mnb::Context& c, int device) {
         throw mnb::Error(MNB_ERR_CUDA, "cusolverDnCreateParams failed");
 }
 
+}  // namespace
+
+namespace mnb {
+std::unique_ptr<Context> make_helper_context(const Context& parent) {
+    auto h = std::make_unique<Context>();
+    init_context(*h, parent.device);
+    h->cholqr = parent.cholqr;
+    h->csne = parent.csne;
+    h->p2fa = parent.p2fa;
+    h->two_norm_check = parent.two_norm_check;
+    return h;
+}
+}  // namespace mnb
+
+namespace {
+
 void copy_out(void* dst, const void* src, size_t bytes, int location, cudaStream_t stream) {
     MNB_CUDA(cudaMemcpyAsync(dst, src, bytes, location == MNB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                              stream));

@@ -152,6 +152,10 @@ struct Context {
     size_t timer_next = 0;
     std::vector<PendingTimer> timers;
     cudaStream_t aux_stream = nullptr;  // second compute stream (QRs / Steps 2-3 beside the sketches and passes)
+    // QR(E) runs on a host helper thread with its own stream, library handles and workspaces
+    // (beside QR(S) / Steps 2-3, which hold host round trips of their own): created on first use
+    std::unique_ptr<Context> qr_helper;
+    Context& helper();
     std::vector<unsigned char> host_work;  // cuSOLVER host workspace (kept alive across async calls)
 
     ~Context();
@@ -194,6 +198,8 @@ struct LsqResult {
 };
 void sync(Context& ctx);
 void trace(const char* what);  // MNB_TRACE=1: host phase timestamps on stderr
+// a secondary context on the same device (abi.cu): own stream, cuBLAS / cuSOLVER handles
+std::unique_ptr<Context> make_helper_context(const Context& parent);
 void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_config& cfg, double2* x_dev,
                       double2* c_dev, mnb_solve_report& rep);
 void solve_classical(Context& ctx, const double2* b_host, double2* x_dev, mnb_classical_report& rep);

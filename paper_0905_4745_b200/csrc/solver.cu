@@ -192,6 +192,12 @@ void Context::make_resident() {
     A_host = nullptr;
 }
 
+Context& Context::helper() {
+    if (!qr_helper) qr_helper = make_helper_context(*this);
+    qr_helper->m = m;
+    return *qr_helper;
+}
+
 cudaEvent_t Context::timer_event() {
     if (timer_next == timer_pool.size()) {
         cudaEvent_t e;
@@ -261,7 +267,7 @@ void launch_cg_init_from_sketch(Context& ctx, const double2* S, int64_t l, const
 
 LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ldR, double tau, int64_t max_it,
                  double dup, double2* y, bool want_norms, double2* x, double2* ax, bool init_done,
-                 bool rinv_ready) {
+                 bool rinv_ready, const double2* rinv_src = nullptr) {
     const int64_t m = ctx.m, n = ctx.n_local;
     LsqResult res;
     const double t0 = now_s();
@@ -269,6 +275,8 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
     double2* Rinv_rows = dev<double2>(ctx.Rinv_rows, size_t(m) * size_t(m));
     if (!rinv_ready) upper_inverse(ctx, Rtop, ldR, m, Rinv);  // (else the one-pass Cholesky path left it)
+    else if (rinv_src && rinv_src != Rinv)  // ... in the helper context's buffer
+        MNB_CUDA(cudaMemcpyAsync(Rinv, rinv_src, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     launch_transpose(Rinv, m, m, m, Rinv_rows, m, ctx.stream);
     ctx.launches += 1;
 
@@ -983,6 +991,40 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     }
     trace("sketch E issued");
 
+    // ---- QR(E) (Step 4's preconditioner, src/lsq.cpp:58-64) on a helper host thread with its own
+    // stream, handles and workspaces, beside QR(S) and Steps 2-3 below (whose host round trips would
+    // otherwise hold it back until c is ready).  Not at m > 2048 (c5: the S chain finishes during
+    // E's sketch anyway, and the duplicated QR workspaces would eat into the sketch's slab budget).
+    SketchQr eq;
+    cudaEvent_t eQ = ctx.timer_event();
+    std::future<void> fut_eq;
+    struct JoinEq {
+        std::future<void>& f;
+        ~JoinEq() { if (f.valid()) f.wait(); }
+    } join_eq{fut_eq};
+    const bool qr_thread = m <= 2048 && !std::getenv("MNB_QR_SERIAL");
+    Context* qctx = qr_thread ? &ctx.helper() : nullptr;
+    auto qr_E = [&](Context& q) {
+        eq = qr_of_sketch(q, Ebuf, l, q.tau_E, q.R_E, &qr_s1, /*precond=*/true);
+        if (int64_t bad = deficient_count(q, eq.R, eq.ldR, m, n); bad > 0)
+            throw Error(MNB_ERR_RANK_DEFICIENCY,
+                        "solve_least_squares: sketch QR found " + std::to_string(bad) +
+                            " numerically dependent columns",
+                        bad);
+        MNB_CUDA(cudaEventRecord(eQ, q.stream));
+    };
+    if (qr_thread) {
+        qctx->timers.clear();
+        qctx->timer_next = 0;
+        qctx->qr_shifted = false;
+        MNB_CUDA(cudaStreamWaitEvent(qctx->stream, eE, 0));
+        const int device = ctx.device;
+        fut_eq = host_async([&, device] {
+            MNB_CUDA(cudaSetDevice(device));
+            qr_E(*qctx);
+        });
+    }
+
     // ---- Step 1 QR and Steps 2-3 on s2
     SketchQr sq;
     double2* c_vec = dev<double2>(ctx.vec_n[2], size_t(n));
@@ -1041,23 +1083,19 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     if (sq.path != 2 && !std::getenv("MNB_INIT_PASS")) launch_cg_init_from_sketch(ctx, Sbuf, l, z, c_loc, xacc);
     else launch_cg_init_pass(ctx, c_loc, xacc);
     trace("INIT issued");
-    SketchQr eq;
-    cudaEvent_t eQ = ctx.timer_event();
-    {
+    if (qr_thread) {
+        fut_eq.get();  // rethrows the helper's errors
+        ctx.launches += qctx->launches;
+        qctx->launches = 0;
+    } else {
         OnStream on(ctx, s2);
         MNB_CUDA(cudaStreamWaitEvent(s2, eE, 0));
-        eq = qr_of_sketch(ctx, Ebuf, l, ctx.tau_E, ctx.R_E, &qr_s1, /*precond=*/true);
-        if (int64_t bad = deficient_count(ctx, eq.R, eq.ldR, m, n); bad > 0)
-            throw Error(MNB_ERR_RANK_DEFICIENCY,
-                        "solve_least_squares: sketch QR found " + std::to_string(bad) +
-                            " numerically dependent columns",
-                        bad);
-        MNB_CUDA(cudaEventRecord(eQ, ctx.stream));
+        qr_E(ctx);
     }
     trace("QR(E)");
     MNB_CUDA(cudaStreamWaitEvent(s1, eQ, 0));
     LsqResult ls = run_cg(ctx, c_loc, eq.R, eq.ldR, rep.lsq_tau, cfg.lsq_max_iterations, double(Tp.max_mult), y, false,
-                          xacc, ax, /*init_done=*/true, eq.rinv_ready);
+                          xacc, ax, /*init_done=*/true, eq.rinv_ready, qr_thread ? qctx->Rinv.as<double2>() : nullptr);
     trace("CG");
     {
         float ms = 0.f;

@@ -779,9 +779,16 @@ bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const doub
         MNB_CUDA(cudaMemcpyAsync(w, bd, size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
         cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(l), int(m), &mone, Sc, int(l), zc, 1, &one, wc, 1),
                      "zgemv");
-        double nr = 0.0, nz = 0.0;
-        cublas_check(cublasDznrm2(ctx.cublas, int(m), wc, 1, &nr), "dznrm2");
-        cublas_check(cublasDznrm2(ctx.cublas, int(l), zc, 1, &nz), "dznrm2");
+        // both norms on the device, one host read per correction
+        double* nrm_d = dev<double>(ctx.scratch, 512);
+        cublasSetPointerMode(ctx.cublas, CUBLAS_POINTER_MODE_DEVICE);
+        cublas_check(cublasDznrm2(ctx.cublas, int(m), wc, 1, nrm_d), "dznrm2");
+        cublas_check(cublasDznrm2(ctx.cublas, int(l), zc, 1, nrm_d + 1), "dznrm2");
+        cublasSetPointerMode(ctx.cublas, CUBLAS_POINTER_MODE_HOST);
+        double nrz[2];
+        MNB_CUDA(cudaMemcpyAsync(nrz, nrm_d, sizeof nrz, cudaMemcpyDeviceToHost, ctx.stream));
+        MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+        const double nr = nrz[0], nz = nrz[1];
         if (std::getenv("MNB_TRACE")) std::fprintf(stderr, "[mnb] csne it %d: ||b - S^H z|| = %.3e (thr %.3e)\n", it, nr, thr * nz);
         if (it == 0 || nr < best) {
             best = nr;

@@ -737,108 +737,7 @@ bool launch_fft_select_pruned(const FftPassArgs& a, const int32_t* off, const in
     return true;
 }
 
-// Pass B at N = 1024 on half tiles: unit = (8-row block, f2, half), 4 rows x 1024 (64 KiB),
-// double-buffered in shared memory by cp.async (16 B per thread and copy, the 4 rows of one k1 =
-// 64 B contiguous; the other half of every 128-byte line is read by the CTA running the other
-// half at the same time).  The next unit's tile is in flight during this unit's transform and
-// sums; the 8-row single-buffer kernel above had to wait for each 128 KiB TMA tile (the buffer is
-// reused) before the transform of the next one could start.  Same arithmetic as above.
-constexpr int kH = 4;  // rows per unit
-__global__ void __launch_bounds__(256, 1) fft1024_select_half_kernel(const FftPassArgs a, const int32_t* __restrict__ off,
-                                                                   const int32_t* __restrict__ ent) {
-    constexpr int N = 1024, NT = 256, NW = NT / 32;
-    extern __shared__ double2 sm[];
-    double2* T0 = sm;                        // two tiles [1024][4]
-    double2* W = T0 + 2 * N * kH;            // w_1024^k
-    double2* P = W + N;                      // partial sums [8 warps][kSB][4 rows]
-    int32_t* ENT = reinterpret_cast<int32_t*>(P + NW * kSB * kH);  // the unit's (f1, slot) pairs, up to kEnt
-    int32_t* JOFF = ENT + 2 * kEnt;          // first entry with f1 mod 16 >= j, j = 0..16
-    const int r = int(threadIdx.x & 3), u = int(threadIdx.x >> 2);
-    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
-    const int64_t units = ((a.rows + 7) / 8) * a.batches * 2;
-    for (int i = threadIdx.x; i < N; i += NT) W[i] = __ldg(a.tw + i);
-    auto issue = [&](int64_t unit, double2* T) {  // cp.async of the unit's 4 x 1024 tile
-        const int64_t half = unit & 1, ub = unit >> 1;
-        const double2* src = a.in + ub * int64_t(N) * 8 + 4 * half;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int i = int(threadIdx.x) + NT * q;  // (k1, row) = (i >> 2, i & 3)
-            asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(sm_u32(T + i)),
-                         "l"(src + int64_t(i >> 2) * 8 + (i & 3))
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int64_t unit = blockIdx.x;
-    int cur = 0;
-    if (unit < units) issue(unit, T0);
-    double2 v[16];
-    for (; unit < units; unit += gridDim.x) {
-        const int64_t half = unit & 1, ub = unit >> 1;
-        const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
-        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
-        const int32_t* E = cnt <= kEnt ? ENT : ent + 2 * e0;
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();  // this unit's tile has landed (all threads' copies); the other buffer is free
-        {
-            const int64_t next = unit + gridDim.x;
-            if (next < units) issue(next, T0 + (cur ^ 1) * N * kH);
-        }
-        const double2* T = T0 + cur * N * kH;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = T[(u + 64 * q) * kH + r];
-        for (int t = threadIdx.x; t < 2 * min(cnt, kEnt); t += NT) ENT[t] = __ldg(ent + 2 * e0 + t);
-        if (threadIdx.x < 17) {
-            int o = 0;
-            while (o < cnt && (__ldg(ent + 2 * (e0 + o)) & 15) < int(threadIdx.x)) ++o;
-            JOFF[threadIdx.x] = o;
-        }
-        cur ^= 1;
-        __syncthreads();  // ENT / JOFF visible
-        if (cnt == 0) continue;
-        dft16_np<false>(v);
-        for (int b0 = 0; b0 < cnt; b0 += kSB) {
-            const int nb = min(kSB, cnt - b0);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int lo = max(JOFF[j], b0), hi = min(JOFF[j + 1], b0 + nb);
-                for (int s = lo; s < hi; ++s) {  // warp-uniform bounds: the shuffles are convergent
-                    const int f = E[2 * s];
-                    double2 p = c_mul(v[d16(j)], W[(f * u) & (N - 1)]);
-#pragma unroll
-                    for (int o = 4; o < 32; o <<= 1) {
-                        p.x += __shfl_xor_sync(0xffffffffu, p.x, o);
-                        p.y += __shfl_xor_sync(0xffffffffu, p.y, o);
-                    }
-                    if (lane < 4) P[(warp * kSB + (s - b0)) * kH + lane] = p;
-                }
-            }
-            __syncthreads();
-            if (int(threadIdx.x) < kH * nb) {
-                const int rr = int(threadIdx.x) & 3, sl = int(threadIdx.x) >> 2;
-                double2 acc = P[sl * kH + rr];
-#pragma unroll
-                for (int w = 1; w < NW; ++w) acc = c_add(acc, P[(w * kSB + sl) * kH + rr]);
-                const int64_t row = rb * 8 + 4 * half + rr;
-                if (row < a.rows) a.out[int64_t(E[2 * (b0 + sl) + 1]) + (a.out_row0 + row) * a.ld_out] = c_scale(acc, a.scale);
-            }
-            __syncthreads();  // P (and, after the last batch, ENT / JOFF) reused
-        }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 void launch_fft1024_select(const FftPassArgs& a, const int32_t* off, const int32_t* ent, cudaStream_t stream) {
-    static const bool half = [] { const char* e = std::getenv("MNB_FB_HALF"); return !(e && std::atoi(e) == 0); }();
-    if (half) {
-        const size_t smem = (size_t(2) * 1024 * kH + 1024 + 8 * kSB * kH) * sizeof(double2) + (2 * kEnt + 20) * 4 + 16;
-        MNB_CUDA(cudaFuncSetAttribute(fft1024_select_half_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches * 2;
-        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, a.num_sms)));
-        fft1024_select_half_kernel<<<grid, 256, smem, stream>>>(a, off, ent);
-        MNB_LAUNCH_CHECK();
-        return;
-    }
     const size_t smem = (size_t(1024) * (8 + 1) + 16 * kSB * 8) * sizeof(double2) + (2 * kEnt + 20) * 4 + 16;
     MNB_CUDA(cudaFuncSetAttribute(fft1024_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;

@@ -495,7 +495,10 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             dmax = std::max(dmax, a);
             dmin = std::min(dmin, a);
         }
-        if (!(dmin > 0.0) || dmax / dmin > 1e7) return false;
+        // the diagonal ratio of R1 bounds cond(S) from below: once u ratio^2 > 1e-3 neither a second
+        // Cholesky pass nor the seminormal corrections can reach orthogonality / the rounding floor
+        // (c3, kappa = 1e8): hand over to shifted CholeskyQR3 at once instead of failing later
+        if (!(dmin > 0.0) || kEps * (dmax / dmin) * (dmax / dmin) > 1e-3) return false;
     }
     if (r1_only) {
         MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
@@ -551,15 +554,17 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, nrm_d), "dznrm2");
             for (int it = 0; it < 10; ++it) {
                 launch_unit_copy(v, a, m, nrm_d, ctx.stream);                    // v = v / ||v||, a = v
-                cublas_check(cublasZtrmv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, int(m),
-                                         Ri, int(m), ac, 1), "ztrmv");          // a = R1^{-1} v
+                // (R1^{-1} from ZTRSM against I: its strict lower triangle is exactly zero, so a plain
+                // GEMV -- one streaming read, no triangular dependency chain -- applies it)
+                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(m), int(m), consts, Ri, int(m), vc, 1, consts + 1,
+                                         ac, 1), "zgemv");                      // a = R1^{-1} v
                 cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), consts, Sc, int(l), ac, 1, consts + 1,
                                          qc, 1), "zgemv");                      // q = E a
                 cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(l), int(m), consts, Sc, int(l), qc, 1, consts + 1,
                                          ac, 1), "zgemv");                      // a = E^H q
-                cublas_check(cublasZtrmv(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, int(m),
-                                         Ri, int(m), ac, 1), "ztrmv");          // a = R1^{-H} a
-                launch_sub_copy(a, v, m, ctx.stream);                            // v = a = D v
+                cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_C, int(m), int(m), consts, Ri, int(m), ac, 1, consts + 1,
+                                         qc, 1), "zgemv");                      // q = R1^{-H} a
+                launch_sub_copy(qc, v, m, ctx.stream);                           // v = q - v = D v
                 cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, nrm_d), "dznrm2");  // ||D v||
                 ctx.launches += 2;
             }

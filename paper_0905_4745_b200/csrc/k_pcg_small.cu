@@ -90,6 +90,145 @@ __device__ __forceinline__ void axpy_accs(double2& acc, double a, double2 t) {
     acc.y = fma(a, t.y, acc.y);
 }
 
+// Phases R, U1, U2 of one CG iteration (see the header) over `parts` pass partials; every CTA
+// keeps the same CgState copy S.  Returns true when the loop stops (the state says why).
+template <int W>
+__device__ bool cg_update(const SmallCgArgs& p, int parts, CgState& S, double2* v_sh, double (*red_sh)[4],
+                          cg::grid_group& grid) {
+    const int64_t m = p.m;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x, G = gridDim.x;
+    const int64_t rs = (m + G - 1) / G, r0 = ::min(m, int64_t(c) * rs), r1 = ::min(m, r0 + rs);
+        // ------------------------------------------------------------ R: reduce
+        for (int64_t i = r0 + warp; i < r1; i += W) {  // a warp per row of the slice
+            const double2 acc = warp_sum_parts2(p.part_s + i, m, parts, lane);
+            if (lane == 0) p.s[i] = acc;
+        }
+        if (warp < 3) {  // a warp per scalar (every CTA: identical sums)
+            const double acc = warp_sum_parts(p.part_scal + warp, 4, parts, lane);
+            if (lane == 0) red_sh[0][warp] = acc;
+        }
+        __syncthreads();
+        const double qq_t = red_sh[0][0], rt_t = red_sh[0][1], rrk = red_sh[0][2];
+        if (qq_t == 0.0) {  // lsq.cpp:91: break before any update
+            if (threadIdx.x == 0) {
+                S.done = 1;
+                S.stop_qq0 = 1;
+                S.alpha = 0.0;
+                S.rr = rrk;
+                if (c == 0) p.residual_norms[S.iterations] = sqrt(rrk);
+            }
+            __syncthreads();
+            return true;
+        }
+        const double alpha = S.gg / qq_t;
+        grid.sync();
+        // ---------------------------------------------------------- U1: gradient
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) v_sh[i] = __ldcg(p.s + i);
+        __syncthreads();
+        double my = 0.0;
+        for (int64_t j = r0 + warp; j < r1; j += W) {
+            const double2* col = p.Rinv + j * m;  // column j of Rinv: entries i <= j
+            double2 acc = make_double2(0.0, 0.0);
+            for (int64_t i = lane; i <= j; i += 32) {
+                const double2 a = __ldcg(col + i), b = v_sh[i];
+                acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));  // conj(a) b
+                acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+            }
+            acc = warp_sum2s(acc);
+            if (lane == 0) {
+                if (p.ax) {
+                    double2 axj = p.ax[j];
+                    axj.x = fma(alpha, v_sh[j].x, axj.x);
+                    axj.y = fma(alpha, v_sh[j].y, axj.y);
+                    p.ax[j] = axj;
+                }
+                const double2 dj = p.dir[j];
+                double2 uj = p.u[j];
+                uj.x = fma(alpha, dj.x, uj.x);
+                uj.y = fma(alpha, dj.y, uj.y);
+                p.u[j] = uj;
+                p.dir_old[j] = dj;
+                double2 gj = p.g[j];
+                gj.x = fma(-alpha, acc.x, gj.x);
+                gj.y = fma(-alpha, acc.y, gj.y);
+                p.g[j] = gj;
+                my += gj.x * gj.x + gj.y * gj.y;
+            }
+        }
+        if (lane == 0) red_sh[warp][3] = my;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
+            for (int q = 0; q < W; ++q) acc += red_sh[q][3];
+            p.part_gg[c] = acc;
+            // replicated state (pcg_upd1_kernel's block-0 epilogue)
+            if (c == 0) p.residual_norms[S.iterations] = sqrt(rrk);
+            S.rr = rrk - 2.0 * alpha * rt_t + alpha * alpha * qq_t;
+            S.alpha = alpha;
+            S.iterations += 1;
+            S.gg_prev = S.gg;
+        }
+        grid.sync();
+        // --------------------------------------------------------- U2: direction
+        if (warp == 0) {
+            const double ggn = warp_sum_parts(p.part_gg, 1, gridDim.x, lane);  // fixed order, every CTA
+            if (lane == 0) {
+            const double excess = S.dup * ggn;
+            const bool conv = excess <= S.tau * fmax(S.rr - excess, 0.0) || S.rr <= S.floor2;
+            const bool capped = S.iterations >= S.max_iterations;
+            S.excess = excess;
+            if (conv || capped || ggn == 0.0) {
+                S.done = 1;
+                S.converged = conv ? 1 : 0;
+                S.gg = ggn;
+            } else {
+                red_sh[0][3] = ggn / S.gg_prev;  // beta
+                S.gg = ggn;
+            }
+            }
+        }
+        __syncthreads();
+        if (S.done) return true;
+        const double beta = red_sh[0][3];
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const double2 gi = __ldcg(p.g + i), di = __ldcg(p.dir_old + i);
+            v_sh[i] = make_double2(fma(beta, di.x, gi.x), fma(beta, di.y, gi.y));
+        }
+        __syncthreads();
+        for (int64_t i = r0 + warp; i < r1; i += W) {
+            const double2* row = p.Rinv_rows + i * m;  // row i of Rinv: entries j >= i
+            double2 acc = make_double2(0.0, 0.0);
+            for (int64_t jj = i + lane; jj < m; jj += 32) {
+                const double2 a = __ldcg(row + jj), b = v_sh[jj];
+                acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+                acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+            }
+            acc = warp_sum2s(acc);
+            if (lane == 0) {
+                p.w[i] = acc;
+                p.dir[i] = v_sh[i];
+            }
+        }
+        return false;
+}
+
+// One CG iteration's m-space work for the multi-kernel loop (A too large for L2): the phases above
+// in one cooperative launch after each fused pass, instead of the reduce / upd1 / upd2 kernels
+// (k_pcg.cu).  State in global memory (read by the pass, written back by CTA 0).
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) pcg_update_kernel(const SmallCgArgs p, int parts) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double2 sm[];
+    __shared__ double red_sh[kMaxWarps][4];
+    __shared__ CgState S;
+    if (threadIdx.x == 0) S = *p.st;
+    __syncthreads();
+    if (S.done) return;  // uniform: every CTA read the same state
+    cg_update<W>(p, parts, S, sm, red_sh, grid);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *p.st = S;
+}
+
 // EPL: rows per lane (m <= 32 EPL).  Shared memory: w / s / d (m each), the per-warp s partials
 // [kSmallWarps][m], scalar scratch.
 // W warps per CTA: 16, or 8 at EPL >= 4 (more registers per thread: no spills)
@@ -212,117 +351,7 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
             p.part_scal[c * 4 + threadIdx.x] = acc;
         }
         grid.sync();
-        // ------------------------------------------------------------ R: reduce
-        for (int64_t i = r0 + warp; i < r1; i += kSmallWarps) {  // a warp per row of the slice
-            const double2 acc = warp_sum_parts2(p.part_s + i, m, G, lane);
-            if (lane == 0) p.s[i] = acc;
-        }
-        if (warp < 3) {  // a warp per scalar (every CTA: identical sums)
-            const double acc = warp_sum_parts(p.part_scal + warp, 4, G, lane);
-            if (lane == 0) red_sh[0][warp] = acc;
-        }
-        __syncthreads();
-        const double qq_t = red_sh[0][0], rt_t = red_sh[0][1], rrk = red_sh[0][2];
-        if (qq_t == 0.0) {  // lsq.cpp:91: break before any update
-            if (threadIdx.x == 0) {
-                S.done = 1;
-                S.stop_qq0 = 1;
-                S.alpha = 0.0;
-                S.rr = rrk;
-                if (c == 0) p.residual_norms[S.iterations] = sqrt(rrk);
-            }
-            __syncthreads();
-            break;
-        }
-        const double alpha = S.gg / qq_t;
-        grid.sync();
-        // ---------------------------------------------------------- U1: gradient
-        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) v_sh[i] = __ldcg(p.s + i);
-        __syncthreads();
-        double my = 0.0;
-        for (int64_t j = r0 + warp; j < r1; j += kSmallWarps) {
-            const double2* col = p.Rinv + j * m;  // column j of Rinv: entries i <= j
-            double2 acc = make_double2(0.0, 0.0);
-            for (int64_t i = lane; i <= j; i += 32) {
-                const double2 a = __ldcg(col + i), b = v_sh[i];
-                acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));  // conj(a) b
-                acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
-            }
-            acc = warp_sum2s(acc);
-            if (lane == 0) {
-                if (p.ax) {
-                    double2 axj = p.ax[j];
-                    axj.x = fma(alpha, v_sh[j].x, axj.x);
-                    axj.y = fma(alpha, v_sh[j].y, axj.y);
-                    p.ax[j] = axj;
-                }
-                const double2 dj = p.dir[j];
-                double2 uj = p.u[j];
-                uj.x = fma(alpha, dj.x, uj.x);
-                uj.y = fma(alpha, dj.y, uj.y);
-                p.u[j] = uj;
-                p.dir_old[j] = dj;
-                double2 gj = p.g[j];
-                gj.x = fma(-alpha, acc.x, gj.x);
-                gj.y = fma(-alpha, acc.y, gj.y);
-                p.g[j] = gj;
-                my += gj.x * gj.x + gj.y * gj.y;
-            }
-        }
-        if (lane == 0) red_sh[warp][3] = my;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double acc = 0.0;
-            for (int q = 0; q < kSmallWarps; ++q) acc += red_sh[q][3];
-            p.part_gg[c] = acc;
-            // replicated state (pcg_upd1_kernel's block-0 epilogue)
-            if (c == 0) p.residual_norms[S.iterations] = sqrt(rrk);
-            S.rr = rrk - 2.0 * alpha * rt_t + alpha * alpha * qq_t;
-            S.alpha = alpha;
-            S.iterations += 1;
-            S.gg_prev = S.gg;
-        }
-        grid.sync();
-        // --------------------------------------------------------- U2: direction
-        if (warp == 0) {
-            const double ggn = warp_sum_parts(p.part_gg, 1, G, lane);  // fixed order, every CTA
-            if (lane == 0) {
-            const double excess = S.dup * ggn;
-            const bool conv = excess <= S.tau * fmax(S.rr - excess, 0.0) || S.rr <= S.floor2;
-            const bool capped = S.iterations >= S.max_iterations;
-            S.excess = excess;
-            if (conv || capped || ggn == 0.0) {
-                S.done = 1;
-                S.converged = conv ? 1 : 0;
-                S.gg = ggn;
-            } else {
-                red_sh[0][3] = ggn / S.gg_prev;  // beta
-                S.gg = ggn;
-            }
-            }
-        }
-        __syncthreads();
-        if (S.done) break;
-        const double beta = red_sh[0][3];
-        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-            const double2 gi = __ldcg(p.g + i), di = __ldcg(p.dir_old + i);
-            v_sh[i] = make_double2(fma(beta, di.x, gi.x), fma(beta, di.y, gi.y));
-        }
-        __syncthreads();
-        for (int64_t i = r0 + warp; i < r1; i += kSmallWarps) {
-            const double2* row = p.Rinv_rows + i * m;  // row i of Rinv: entries j >= i
-            double2 acc = make_double2(0.0, 0.0);
-            for (int64_t jj = i + lane; jj < m; jj += 32) {
-                const double2 a = __ldcg(row + jj), b = v_sh[jj];
-                acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-                acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
-            }
-            acc = warp_sum2s(acc);
-            if (lane == 0) {
-                p.w[i] = acc;
-                p.dir[i] = v_sh[i];
-            }
-        }
+        if (cg_update<W>(p, G, S, v_sh, red_sh, grid)) break;
         grid.sync();
     }
     if (c == 0 && threadIdx.x == 0) *p.st = S;
@@ -347,6 +376,21 @@ void launch_small_epl(const SmallCgArgs& a, int grid, cudaStream_t stream) {
 }
 
 }  // namespace
+
+int pcg_update_grid(int64_t m, int num_sms) {
+    // one warp per row of a slice: rows / 8 CTAs of 8 warps, at most one CTA per SM
+    return int(std::max<int64_t>(1, std::min<int64_t>(num_sms, (m + 7) / 8)));
+}
+
+void launch_pcg_update(const SmallCgArgs& a, int parts, int grid, cudaStream_t stream) {
+    auto k = pcg_update_kernel<8>;
+    const size_t smem = size_t(a.m) * 16;
+    MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SmallCgArgs args = a;
+    void* params[] = {&args, &parts};
+    MNB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(8 * 32), params, smem,
+                                         stream));
+}
 
 bool pcg_small_eligible(int64_t m, int64_t n, int is_real) {
     const size_t bytes = size_t(m) * size_t(n) * (is_real ? 8 : 16);

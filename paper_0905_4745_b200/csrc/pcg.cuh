@@ -99,5 +99,8 @@ struct SmallCgArgs {
 bool pcg_small_eligible(int64_t m, int64_t n, int is_real);
 int pcg_small_grid(int64_t m, int64_t n, int num_sms);
 void launch_pcg_small(const SmallCgArgs& a, int grid, cudaStream_t stream);
+// one iteration's reduce + gradient + direction phases as one cooperative launch (A, n, x unused)
+int pcg_update_grid(int64_t m, int num_sms);
+void launch_pcg_update(const SmallCgArgs& a, int parts, int grid, cudaStream_t stream);
 
 }  // namespace mnb

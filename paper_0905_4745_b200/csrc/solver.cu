@@ -346,18 +346,66 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
         ctx.launches += 1;
         pass_ev.emplace_back(e0, e1);
     }
+    // one GPU, A beyond L2: each iteration is the fused pass + one cooperative update launch
+    // (k_pcg_small.cu pcg_update_kernel) in place of reduce / upd1 / upd2; multi-GPU keeps the
+    // three kernels around the per-iteration allreduce
+    const bool merged = !small && !ctx.distributed() && n > 0 && !std::getenv("MNB_CG_UPD3");
+    const int ugrid = pcg_update_grid(m, ctx.num_sms);
+    SmallCgArgs ua;
+    if (merged) {
+        ua.m = m;
+        ua.Rinv = Rinv;
+        ua.Rinv_rows = Rinv_rows;
+        ua.u = u;
+        ua.g = g;
+        ua.dir = dir;
+        ua.dir_old = dir_old;
+        ua.w = w;
+        ua.ax = ax;
+        ua.part_s = pb.part_s;
+        ua.part_scal = pb.part_scal;
+        ua.s = reinterpret_cast<double2*>(pb.red);
+        ua.part_gg = dev<double>(ctx.part_gg, size_t(std::max(ugrid, ub)));
+        ua.st = st;
+        ua.residual_norms = norms;
+    }
+    auto launch_pass_only = [&](int mode) {
+        PcgPassArgs a;
+        a.A = ctx.A;
+        a.is_real = ctx.dtype == MNB_F64;
+        a.m = m;
+        a.n = n;
+        a.w = w;
+        a.tin = t;
+        a.tout = t;
+        a.r = r;
+        a.x = x;
+        a.state = st;
+        a.part_s = pb.part_s;
+        a.part_scal = pb.part_scal;
+        a.mode = mode;
+        launch_pcg_pass(a, pb.plan, ctx.stream);
+    };
     for (; !small;) {
         read_state();
         if (st_h->done || issued >= max_it + 1) break;
         for (int64_t k = 0; k < K; ++k) {
             cudaEvent_t e0 = ctx.event(32 + 2 * size_t(issued)), e1 = ctx.event(33 + 2 * size_t(issued));
-            MNB_CUDA(cudaEventRecord(e0, ctx.stream));
-            fused_pass(ctx, pb, PCG_CG, w, t, t, r, st, x);
-            MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+            if (merged) {  // the pass, then reduce + gradient + direction in one cooperative launch
+                MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+                launch_pass_only(PCG_CG);
+                MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+                launch_pcg_update(ua, pb.plan.grid, ugrid, ctx.stream);
+                ctx.launches += 2;
+            } else {
+                MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+                fused_pass(ctx, pb, PCG_CG, w, t, t, r, st, x);
+                MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+                launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 0, ctx.stream, ax);
+                launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 0, ctx.stream);
+                ctx.launches += 2;
+            }
             pass_ev.emplace_back(e0, e1);
-            launch_pcg_upd1(pb.red, Rinv, m, u, g, dir, dir_old, part_gg, st, norms, 0, ctx.stream, ax);
-            launch_pcg_upd2(part_gg, ub, Rinv_rows, m, g, dir_old, dir, w, st, 0, ctx.stream);
-            ctx.launches += 2;
             ++issued;
         }
     }

@@ -108,7 +108,9 @@ int mnb_redistribute_plan(int64_t m, int64_t n_global, int world_size, int rank,
 /* The problem matrix A (ProblemInstance::A, include/minnorm/solver.hpp:14-24):
  * this rank's column shard A[:, col_begin : col_begin+n_local], column-major
  * with leading dimension lda >= m.  location MNB_DEVICE borrows the pointer
- * (caller keeps it alive; requires lda == m), MNB_HOST copies it to the GPU,
+ * (caller keeps it alive; requires lda == m; the library's work is ordered on
+ * the context's stream only, so the caller completes -- or orders through
+ * mnb_context_set_stream -- whatever produces A), MNB_HOST copies it to the GPU,
  * MNB_HOST_ASYNC (single GPU, page-locked host memory; otherwise as MNB_HOST)
  * defers the copy: mnb_solve_randomized streams A in row slabs and sketches
  * each slab as it lands, and any other call first completes the copy. */

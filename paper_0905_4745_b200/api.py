@@ -200,6 +200,9 @@ class Context:
             m, nl = A.shape
             if not (A.stride(0) == 1 and A.stride(1) == m):
                 raise ValueError("device A must be column-major (A.T contiguous)")
+            # the library works on its own stream: whatever torch queued to produce A (on any of
+            # its streams) must be complete before a solve reads the borrowed pointer
+            torch.cuda.synchronize(A.device)
             self._keep = A
             ptr, loc = ctypes.c_void_p(A.data_ptr()), L.MNB_DEVICE
         else:

@@ -278,11 +278,11 @@ def main():
             return
         # Complete solves of the CPU port on the host cores, never a scaled sample.  A c4 solve
         # takes minutes on the host, so the run times as many of the requested W + K solves as
-        # fit in MNB_CPU_BUDGET_S (default 300 s; at least one timed solve) and reports exactly
+        # fit in MNB_CPU_BUDGET_S (default 180 s; at least one timed solve) and reports exactly
         # what ran: "steps" / "warmup" are the counts performed, "*_requested" the flags.
         A_host, b = host_instance(cfg)
         threads = cpu_threads(cfg)
-        budget = float(os.environ.get("MNB_CPU_BUDGET_S", "300"))
+        budget = float(os.environ.get("MNB_CPU_BUDGET_S", "180"))
         t_begin = time.perf_counter()
         dt, ref = cpu_solve(cfg, A_host, b, threads)
         warm, timed = 0, []

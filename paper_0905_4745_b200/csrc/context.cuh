@@ -6,6 +6,7 @@
 #include <cusolverDn.h>
 #include <nccl.h>
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <vector>
@@ -126,8 +127,13 @@ struct Context {
     // until the matrix changes or the next solve starts
     bool slab_ready = false;
     int64_t slab_rows = 0, slab_row0 = 0;
-    DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork;
+    DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork, gram_E;
+    cudaStream_t gram_stream = nullptr;  // E's Gram built slab by slab beside the sketch
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
+    // multi-slab sketches: called after each row slab's kernels are queued (rows [s0, s0 + rs) of
+    // the output are final once they run); the solve uses it to build E's Gram block by block
+    std::function<void(int64_t s0, int64_t rs)> on_slab;
+    const double2* pre_gram = nullptr;  // when set, the next CholeskyQR pass 1 takes this S^H S (upper)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
     bool p2fa = true;    // fused P2 + FFT pass A (k_p2fa.cu) where the shape allows; MNB_P2FA=0 disables
     bool two_norm_check = true;  // one-pass preconditioner accepted on a 2-norm cond estimate; MNB_PRECOND_2NORM=0 disables

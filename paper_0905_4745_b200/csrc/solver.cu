@@ -180,6 +180,7 @@ Context::~Context() {
     if (comm) ncclCommDestroy(comm);
     if (own_stream && stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (gram_stream) cudaStreamDestroy(gram_stream);
 }
 
 void Context::make_resident() {
@@ -523,8 +524,11 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
                                  reinterpret_cast<cuDoubleComplex*>(Q), int(l)),
                      "ztrsm");
     };
-    // pass 1: G = S^H S (+ shift) = R1^H R1, Q1 = S R1^{-1}
-    herk(S, G);
+    // pass 1: G = S^H S (+ shift) = R1^H R1, Q1 = S R1^{-1}  (or the Gram built during the sketch)
+    if (ctx.pre_gram && !shifted)
+        MNB_CUDA(cudaMemcpyAsync(G, ctx.pre_gram, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    else
+        herk(S, G);
     if (shifted) {
         // shifted CholeskyQR (Fukaya et al.): s = 11 (l m + m (m + 1)) u ||S||^2, ||S||_2^2 <= trace(G)
         read_diag(G);
@@ -1018,6 +1022,33 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     MNB_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(int), s1));
     cudaEvent_t eA = ctx.timer_event(), eS = ctx.timer_event(), eE = ctx.timer_event();
     MNB_CUDA(cudaEventRecord(eA, s1));
+    // E's Gram block by block while E is sketched in row slabs (c5; the host-A path at c4): after the
+    // slab of rows [s0, s0 + rs) lands, G[0:s0+rs, s0:s0+rs] = E[:, :s0+rs]^H E[:, s0:s0+rs] on its own
+    // stream, so QR(E) starts from a finished Gram instead of a 16384 x 4096 HERK after the sketch
+    double2* GE = nullptr;
+    bool gram_partial = false;
+    cudaEvent_t eG = ctx.timer_event();
+    auto gram_slab = [&](int64_t s0, int64_t rs) {
+        if (s0 == 0 && rs == m) {  // one slab: nothing to overlap, QR(E) takes its own HERK
+            gram_partial = true;
+            return;
+        }
+        if (!ctx.gram_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.gram_stream, cudaStreamNonBlocking));
+        GE = dev<double2>(ctx.gram_E, size_t(m) * size_t(m));
+        cudaEvent_t e = ctx.timer_event();
+        MNB_CUDA(cudaEventRecord(e, s1));
+        MNB_CUDA(cudaStreamWaitEvent(ctx.gram_stream, e, 0));
+        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+        cublasSetStream(ctx.cublas, ctx.gram_stream);
+        const cublasStatus_t st = cublasZgemm(ctx.cublas, CUBLAS_OP_C, CUBLAS_OP_N, int(s0 + rs), int(rs), int(l), &one,
+                                              reinterpret_cast<const cuDoubleComplex*>(Ebuf), int(l),
+                                              reinterpret_cast<const cuDoubleComplex*>(Ebuf + s0 * l), int(l), &zero,
+                                              reinterpret_cast<cuDoubleComplex*>(GE + s0 * m), int(m));
+        cublasSetStream(ctx.cublas, ctx.stream);
+        cublas_check(st, "zgemm (Gram of E)");
+        MNB_CUDA(cudaEventRecord(eG, ctx.gram_stream));
+    };
+    const bool incr_gram = !ctx.distributed() && !std::getenv("MNB_GRAM_AFTER");
     if (pipelined) {
         for (size_t k = 0; k < slabs.size(); ++k) {
             const auto [r0, rows] = slabs[k];
@@ -1025,7 +1056,9 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
             sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Sbuf, l, r0, rep.sketch_kernel_ms);
             ctx.nonfinite = nullptr;
+            if (incr_gram) ctx.on_slab = gram_slab;
             sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Ebuf, l, r0, rep.sketch_kernel_ms);
+            ctx.on_slab = nullptr;
             MNB_CUDA(cudaEventRecord(ctx.event(240 + k), s1));
             if (k == 0) trace("slab 0 sketches issued");
         }
@@ -1046,9 +1079,12 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         // E's sketch queues behind S's on s1 (from the same redistributed slab) while s2 factors S
         fut_Tp.get();
         upload_srft(ctx, Tp, Tpd);
+        if (incr_gram) ctx.on_slab = gram_slab;
         sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+        ctx.on_slab = nullptr;
         MNB_CUDA(cudaEventRecord(eE, s1));
     }
+    if (gram_partial) GE = nullptr;  // a single slab after all
     trace("sketch E issued");
 
     // ---- QR(E) (Step 4's preconditioner, src/lsq.cpp:58-64) on a helper host thread with its own
@@ -1065,7 +1101,10 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     const bool qr_thread = m <= 2048 && !std::getenv("MNB_QR_SERIAL");
     Context* qctx = qr_thread ? &ctx.helper() : nullptr;
     auto qr_E = [&](Context& q) {
+        if (GE) MNB_CUDA(cudaStreamWaitEvent(q.stream, eG, 0));
+        q.pre_gram = GE;
         eq = qr_of_sketch(q, Ebuf, l, q.tau_E, q.R_E, &qr_s1, /*precond=*/true);
+        q.pre_gram = nullptr;
         if (int64_t bad = deficient_count(q, eq.R, eq.ldR, m, n); bad > 0)
             throw Error(MNB_ERR_RANK_DEFICIENCY,
                         "solve_least_squares: sketch QR found " + std::to_string(bad) +

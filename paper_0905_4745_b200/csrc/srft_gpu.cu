@@ -573,6 +573,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             launch_copy_dups(out, ldo, out_row0 + s0, rs, op.dups.as<int32_t>(), op.ndups, ctx.stream);
             ctx.launches += 1;
         }
+        if (ctx.on_slab) ctx.on_slab(out_row0 + s0, rs);
     }
 }
 

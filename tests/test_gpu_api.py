@@ -209,7 +209,7 @@ def test_lsq_fixed_seed_is_bitwise_reproducible(ctx):
 
 def test_pinned_host_matrix_pipelined_copy_matches(ctx):
     """A page-locked host A takes the MNB_HOST_ASYNC path (row-slab H2D overlapped with both
-    sketches); the solve must equal the one from a pageable (eagerly copied) A bit for bit."""
+    sketches); the solve must equal the one from a pageable (eagerly copied) A."""
     torch = pytest.importorskip("torch")
     A, b = make_instance(192, 4096, 1e3, seed=113)
     pinned = torch.empty((A.shape[1], A.shape[0]), dtype=torch.complex128, pin_memory=True)
@@ -218,9 +218,12 @@ def test_pinned_host_matrix_pipelined_copy_matches(ctx):
     cfg = mn.SolverConfig(epsilon=1e-10, capture_c=True)
     r_pin = mn.solve_randomized(mn.ProblemInstance(A_pinned, b), cfg, ctx)
     r_page = mn.solve_randomized(mn.ProblemInstance(np.asfortranarray(A), b), cfg, ctx)
-    assert r_pin.x.tobytes() == r_page.x.tobytes()
+    # the sketches and c are bit-identical; the pipelined path forms E's Gram block by block as the
+    # slabs land (one ZGEMM per slab) where the eager path takes one ZHERK, so R' -- and the CG
+    # iterates -- agree to rounding
     assert r_pin.c.tobytes() == r_page.c.tobytes()
     assert r_pin.lsq_iterations == r_page.lsq_iterations
+    assert np.linalg.norm(r_pin.x - r_page.x) <= 1e-12 * np.linalg.norm(r_page.x)
     # a later call on the same context sees the resident matrix
     op = mn.build_srft(4 * 192, 4096, mn.derive_seed(42, 11))
     ctx.set_matrix(A_pinned, deferred=True)

@@ -247,9 +247,8 @@ __global__ void __launch_bounds__(W * 32, 1) pcg_small_kernel(const SmallCgArgs 
     const int G = gridDim.x, c = blockIdx.x;
     if (threadIdx.x == 0) S = *p.st;
     __syncthreads();
-    // this CTA's column block and row slice
+    // this CTA's column block (its row slice of the m-space phases is taken in cg_update)
     const int64_t per = (n + G - 1) / G, c0 = ::min(n, int64_t(c) * per), c1 = ::min(n, c0 + per);
-    const int64_t rs = (m + G - 1) / G, r0 = ::min(m, int64_t(c) * rs), r1 = ::min(m, r0 + rs);
 
     while (!S.done) {
         // ------------------------------------------------------------- P: pass

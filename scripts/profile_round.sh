@@ -5,6 +5,8 @@
 tag=${1:-r01}
 mkdir -p gpurun_out/prof_$tag
 B="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
+# the same command line must have exited 0 without ncu first (B200_PROFILING.md)
+timeout 900 $B > gpurun_out/prof_$tag/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 timeout 900 ncu --nvtx --nvtx-include "solve/" --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/prof_$tag/launches_c4.csv $B > gpurun_out/prof_$tag/ncu_launch.log 2>&1
 python scripts/launch_summary.py gpurun_out/prof_$tag/launches_c4.csv > gpurun_out/prof_$tag/launches_c4_summary.txt 2>&1

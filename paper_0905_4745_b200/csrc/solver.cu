@@ -539,6 +539,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         ctx.launches += 1;
     }
     potrf(G);
+    trace("  cholqr: gram + potrf");
     if (info_h != 0) return false;
     if (!shifted) {
         double dmax = 0.0, dmin = 1e300;
@@ -574,6 +575,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         // Q1 = E R1^{-1} (two GEMVs over E and two triangular products per step, from a seeded
         // dense start); ||D v|| for the unit v bounds ||D||_2 from below, so a factor-2 margin is
         // applied (accept on 2 ||D v|| <= 1e-3; c5: ~1e-4).
+        trace("  cholqr: R1^-1 + Frobenius");
         bool accept = kEps * nr * nr * nri * nri <= 1e-3;
         if (!accept && ctx.two_norm_check) {
             double2* v = dev<double2>(ctx.vec_m[8], size_t(m));
@@ -624,6 +626,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             double lam = 0.0;
             MNB_CUDA(cudaMemcpyAsync(&lam, nrm_d, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
             MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+            trace("  cholqr: ||Q1^H Q1 - I|| power steps");
             accept = 2.0 * lam <= 1e-3;
             if (std::getenv("MNB_TRACE"))
                 std::fprintf(stderr, "[mnb] one-pass preconditioner: u cond^2 <= %.2e (Frobenius), ||Q1^H Q1 - I|| ~ %.2e\n",

@@ -125,10 +125,10 @@ EPS_MACH = np.finfo(float).eps
 
 
 def solve_tol(eps, kappa):
-    """What a backward-stable solver can promise: 10*eps (north_star), but not
-    below the conditioning floor ~ eps_mach * kappa (SURVEY §8c measured
-    6e-9 between two exact solvers at kappa = 1e8)."""
-    return max(10 * eps, 10 * EPS_MACH * kappa)
+    """10*eps (north_star), but not below the conditioning floor eps_mach * kappa, where
+    float64 itself stops determining p (SURVEY §8c measured 6e-9 between two exact solvers
+    at kappa = 1e8).  Every case below except the kappa = 1e8 ones is held to 10*eps."""
+    return max(10 * eps, EPS_MACH * kappa)
 
 
 @pytest.mark.parametrize("m,n,kappa,eps", [(64, 1024, 1e3, 1e-12), (256, 16384, 1e6, 1e-10), (16, 256, 1e2, 1e-8),
@@ -143,7 +143,7 @@ def test_solve_randomized_matches_oracle(ctx, m, n, kappa, eps):
     ref = O.solve_randomized(A, b, epsilon=eps, seed=42)
     if ref.lsq_converged:
         # the reference converged: match its x and its iteration count
-        assert rel(rep.x, ref.x) <= 10 * eps + 2 * rel(ref.x, p)
+        assert rel(rep.x, ref.x) <= 10 * eps
         assert abs(rep.lsq_iterations - ref.lsq_iterations) <= 1
         assert abs(rep.c_norm_ratio - ref.c_norm_ratio) <= 1e-8 * ref.c_norm_ratio
     else:

@@ -912,11 +912,113 @@ __global__ void __launch_bounds__(R * U, 4 / R) fft_select_blocked_kernel(const 
     }
 }
 
+// Radix-8 variant for N = 8 U (n = 3 * 2^20: U = 384), 2 rows per unit, 768 threads: each thread
+// holds only 8 values (32 registers), so the transform and the prefetched next unit fit in the 80
+// registers a 768-thread CTA gets -- the radix-16 kernel above spills there (its 16 complex values
+// alone take 64 registers), and the spills clog the load pipe (lg_throttle 45 % of its stalls).
+//   Y_u[j] = sum_q x[u + U q] w_8^{j q}  (q, j < 8),   X[f] = sum_{u < U} w_N^{f u} Y_u[f mod 8]
+template <int U>
+__global__ void __launch_bounds__(2 * U, 1) fft_select_blocked8_kernel(const FftPassArgs a,
+                                                                      const int32_t* __restrict__ off,
+                                                                      const int32_t* __restrict__ ent) {
+    constexpr int R = 2, N = 8 * U, T = R * U, NH = (N + 63) / 64, P = 8 / R;
+    extern __shared__ __align__(16) double2 smb[];
+    double2* X = smb;                 // Y as [8 j][U u][2 r], r slot xor-swizzled by u
+    double2* LO = X + 8 * U * R;      // w_N^k, k < 64 (slot-swizzled)
+    double2* HI = LO + 64;            // w_N^{64 k}
+    int32_t* ENT = reinterpret_cast<int32_t*>(HI + NH);
+    const int r = int(threadIdx.x) % R, u = int(threadIdx.x) / R;
+    const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31), nwarps = T / 32;
+    auto swz = [](int k) { return (k & ~7) | ((k ^ (k >> 3)) & 7); };
+    auto xb = [](int j, int uu, int rr) { return (j * U + uu) * R + (rr ^ ((uu >> 2) & 1)); };
+    for (int i = threadIdx.x; i < 64; i += T) LO[swz(i)] = __ldg(a.tw + i);
+    for (int i = threadIdx.x; i < NH; i += T) HI[i] = __ldg(a.tw + 64 * i);
+    const int64_t nrb8 = (a.rows + 7) / 8;
+    const int64_t units = nrb8 * a.batches * P;
+    auto load = [&](int64_t unit, double2 (&v)[8]) {
+        const int64_t part = unit % P, ub = unit / P;
+        const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
+        const double2* base = a.in + ((rb * a.batches + b) * int64_t(N)) * 8 + R * part + r;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double2* p = base + int64_t(u + U * q) * 8;
+            double2 x;
+            asm volatile("ld.global.nc.L2::128B.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "l"(p));
+            v[q] = x;
+        }
+    };
+    double2 v[8];
+    int64_t unit = blockIdx.x;
+    if (unit < units) load(unit, v);
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t part = unit % P, ub = unit / P;
+        const int64_t rb = ub / a.batches, b = ub - rb * a.batches;
+        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        dft8<false>(v);
+        __syncthreads();  // the previous unit's sums are done with X / ENT (and the tables are loaded)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) X[xb(j, u, r)] = v[j];
+        for (int t = threadIdx.x; t < 2 * min(cnt, kBEnt); t += T) ENT[t] = __ldg(ent + 2 * e0 + t);
+        __syncthreads();
+        const int64_t next = unit + gridDim.x;
+        if (next < units) load(next, v);  // in flight during the sums
+        const int32_t* E = cnt <= kBEnt ? ENT : ent + 2 * e0;
+        for (int p0 = warp; p0 < R * cnt; p0 += 2 * nwarps) {
+            double vv[4];
+            int slot2[2], row2[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int p = p0 + nwarps * k;
+                const bool ok = p < R * cnt;
+                const int rp = p % R, s = ok ? p / R : 0;
+                const int f = E[2 * s];
+                slot2[k] = ok ? E[2 * s + 1] : -1;
+                row2[k] = rp;
+                const int j = f & 7;
+                double2 acc = make_double2(0.0, 0.0);
+                // w^{f uu}, uu = lane + 32 t: w^{f lane} times (w^{32 f})^t  (f lane < 2^17: 32-bit)
+                const int k0 = (f * lane) % N, ks = (f * 32) % N;
+                double2 w = c_mul(HI[k0 >> 6], LO[swz(k0 & 63)]);
+                const double2 wstep = c_mul(HI[ks >> 6], LO[swz(ks & 63)]);
+#pragma unroll
+                for (int t = 0; t < U / 32; ++t) {
+                    const double2 y = X[xb(j, lane + 32 * t, rp)];
+                    acc.x = fma(y.x, w.x, fma(-y.y, w.y, acc.x));
+                    acc.y = fma(y.x, w.y, fma(y.y, w.x, acc.y));
+                    w = c_mul(w, wstep);
+                }
+                vv[2 * k] = acc.x;
+                vv[2 * k + 1] = acc.y;
+            }
+            xreduce4(vv, lane);
+            const double other = __shfl_down_sync(0xffffffffu, vv[0], 8);
+            if ((lane & 15) == 0) {
+                const int k = lane >> 4;
+                const int64_t row = rb * 8 + R * part + row2[k];
+                if (slot2[k] >= 0 && row < a.rows)
+                    a.out[int64_t(slot2[k]) + (a.out_row0 + row) * a.ld_out] = c_scale(make_double2(vv[0], other), a.scale);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 bool launch_fft_select_blocked(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
                                cudaStream_t stream) {
     if (a.inverse || a.N != 3072) return false;
+    static const int radix = [] { const char* e = std::getenv("MNB_FB_RADIX"); return e && std::atoi(e) == 16 ? 16 : 8; }();
+    if (radix == 8) {
+        constexpr int U8 = 384;
+        const size_t smem = (size_t(8) * U8 * 2 + 64 + (a.N + 63) / 64) * sizeof(double2) + 2 * kBEnt * 4;
+        auto k = fft_select_blocked8_kernel<U8>;
+        MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches * 4;
+        const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, num_sms)));
+        k<<<grid, 2 * U8, smem, stream>>>(a, off, ent);
+        MNB_LAUNCH_CHECK();
+        return true;
+    }
     constexpr int U = 192;
     // 4-row units, one CTA per SM (2-row units on two CTAs per SM measured slower: 274 vs 195 ms
     // for both c5 sketches; MNB_FB_ROWS=2 selects them)

@@ -161,5 +161,7 @@ def test_multislab_solve_matches_default():
 
     d = solve()
     s = _with_env("MNB_SLAB_ROWS", "16", solve)
+    # the sketches are bit-identical; with several slabs E's Gram is built block by block (one ZGEMM
+    # per slab) where one slab takes a ZHERK, so R' and the CG iterates agree to rounding
     assert s.lsq_iterations == d.lsq_iterations
-    assert _rel(s.x, d.x) <= 1e-14
+    assert _rel(s.x, d.x) <= 1e-12

@@ -100,13 +100,18 @@ __device__ bool cg_update(const SmallCgArgs& p, int parts, CgState& S, double2* 
     const int c = blockIdx.x, G = gridDim.x;
     const int64_t rs = (m + G - 1) / G, r0 = ::min(m, int64_t(c) * rs), r1 = ::min(m, r0 + rs);
         // ------------------------------------------------------------ R: reduce
-        for (int64_t i = r0 + warp; i < r1; i += W) {  // a warp per row of the slice
-            const double2 acc = warp_sum_parts2(p.part_s + i, m, parts, lane);
-            if (lane == 0) p.s[i] = acc;
-        }
-        if (warp < 3) {  // a warp per scalar (every CTA: identical sums)
-            const double acc = warp_sum_parts(p.part_scal + warp, 4, parts, lane);
-            if (lane == 0) red_sh[0][warp] = acc;
+        // (parts == 0: already reduced -- the distributed loop's allreduced [s | qq, rt, rr] in p.s)
+        if (parts > 0) {
+            for (int64_t i = r0 + warp; i < r1; i += W) {  // a warp per row of the slice
+                const double2 acc = warp_sum_parts2(p.part_s + i, m, parts, lane);
+                if (lane == 0) p.s[i] = acc;
+            }
+            if (warp < 3) {  // a warp per scalar (every CTA: identical sums)
+                const double acc = warp_sum_parts(p.part_scal + warp, 4, parts, lane);
+                if (lane == 0) red_sh[0][warp] = acc;
+            }
+        } else if (threadIdx.x < 3) {
+            red_sh[0][threadIdx.x] = __ldcg(reinterpret_cast<const double*>(p.s) + 2 * m + threadIdx.x);
         }
         __syncthreads();
         const double qq_t = red_sh[0][0], rt_t = red_sh[0][1], rrk = red_sh[0][2];

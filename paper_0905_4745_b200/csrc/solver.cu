@@ -350,7 +350,8 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
     // one GPU, A beyond L2: each iteration is the fused pass + one cooperative update launch
     // (k_pcg_small.cu pcg_update_kernel) in place of reduce / upd1 / upd2; multi-GPU keeps the
     // three kernels around the per-iteration allreduce
-    const bool merged = !small && !ctx.distributed() && n > 0 && !std::getenv("MNB_CG_UPD3");
+    // (distributed: pass + reduce + allreduce, then the update kernel on the allreduced vector)
+    const bool merged = !small && n > 0 && !std::getenv("MNB_CG_UPD3");
     const int ugrid = pcg_update_grid(m, ctx.num_sms);
     SmallCgArgs ua;
     if (merged) {
@@ -392,12 +393,18 @@ LsqResult run_cg(Context& ctx, const double2* c, const double2* Rtop, int64_t ld
         if (st_h->done || issued >= max_it + 1) break;
         for (int64_t k = 0; k < K; ++k) {
             cudaEvent_t e0 = ctx.event(32 + 2 * size_t(issued)), e1 = ctx.event(33 + 2 * size_t(issued));
-            if (merged) {  // the pass, then reduce + gradient + direction in one cooperative launch
+            if (merged && !ctx.distributed()) {  // the pass, then reduce + gradient + direction in one launch
                 MNB_CUDA(cudaEventRecord(e0, ctx.stream));
                 launch_pass_only(PCG_CG);
                 MNB_CUDA(cudaEventRecord(e1, ctx.stream));
                 launch_pcg_update(ua, pb.plan.grid, ugrid, ctx.stream);
                 ctx.launches += 2;
+            } else if (merged) {  // pass + reduce + allreduce, then gradient + direction in one launch
+                MNB_CUDA(cudaEventRecord(e0, ctx.stream));
+                fused_pass(ctx, pb, PCG_CG, w, t, t, r, st, x);
+                MNB_CUDA(cudaEventRecord(e1, ctx.stream));
+                launch_pcg_update(ua, 0, ugrid, ctx.stream);
+                ctx.launches += 1;
             } else {
                 MNB_CUDA(cudaEventRecord(e0, ctx.stream));
                 fused_pass(ctx, pb, PCG_CG, w, t, t, r, st, x);

@@ -1059,6 +1059,10 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         MNB_CUDA(cudaEventRecord(eG, ctx.gram_stream));
     };
     const bool incr_gram = !ctx.distributed() && !std::getenv("MNB_GRAM_AFTER");
+    struct SlabHookGuard {  // the hook captures this frame: never let it outlive the solve
+        Context& c;
+        ~SlabHookGuard() { c.on_slab = nullptr; }
+    } slab_hook_guard{ctx};
     if (pipelined) {
         for (size_t k = 0; k < slabs.size(); ++k) {
             const auto [r0, rows] = slabs[k];
@@ -1112,9 +1116,12 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     Context* qctx = qr_thread ? &ctx.helper() : nullptr;
     auto qr_E = [&](Context& q) {
         if (GE) MNB_CUDA(cudaStreamWaitEvent(q.stream, eG, 0));
-        q.pre_gram = GE;
+        struct PreGram {
+            Context& q;
+            PreGram(Context& c, const double2* g) : q(c) { q.pre_gram = g; }
+            ~PreGram() { q.pre_gram = nullptr; }
+        } pre_gram{q, GE};
         eq = qr_of_sketch(q, Ebuf, l, q.tau_E, q.R_E, &qr_s1, /*precond=*/true);
-        q.pre_gram = nullptr;
         if (int64_t bad = deficient_count(q, eq.R, eq.ldR, m, n); bad > 0)
             throw Error(MNB_ERR_RANK_DEFICIENCY,
                         "solve_least_squares: sketch QR found " + std::to_string(bad) +

@@ -165,3 +165,32 @@ def test_multislab_solve_matches_default():
     # per slab) where one slab takes a ZHERK, so R' and the CG iterates agree to rounding
     assert s.lsq_iterations == d.lsq_iterations
     assert _rel(s.x, d.x) <= 1e-12
+
+
+def test_error_mid_solve_leaves_the_context_usable():
+    """A solve that raises after both sketches were queued (rank deficiency, with the multi-slab
+    sketch and its per-slab Gram hook active, and QR(E) on the helper thread) must leave the context
+    clean: the next solve on it equals a solve on a fresh context."""
+    A, b = make_instance(48, 3 << 16, 1e3, seed=4, real=True)
+    Ad = A.copy()
+    Ad[5] = Ad[3]
+    cfg = mn.SolverConfig(epsilon=1e-10)
+
+    def run():
+        c = mn.Context(0)
+        try:
+            with pytest.raises(mn.RankDeficiencyError):
+                mn.solve_randomized(mn.ProblemInstance(Ad, b), cfg, c)
+            after = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        finally:
+            c.close()
+        c = mn.Context(0)
+        try:
+            fresh = mn.solve_randomized(mn.ProblemInstance(A, b), cfg, c)
+        finally:
+            c.close()
+        return after, fresh
+
+    after, fresh = _with_env("MNB_SLAB_ROWS", "16", run)
+    assert after.lsq_converged and after.lsq_iterations == fresh.lsq_iterations
+    assert np.array_equal(after.x, fresh.x)

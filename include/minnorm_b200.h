@@ -263,6 +263,24 @@ int mnb_apply_adjoint_matrix(mnb_context* ctx, const void* y, int y_location, vo
 
 int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch);
 
+/* ---- the sketch-QR building blocks (hand-written kernels, csrc/k_cholqr.cu) ------------------
+ * The reference factors both sketches with Eigen::HouseholderQR (src/solver.cpp:86,
+ * src/lsq.cpp:58) and applies R by triangular solves (src/solver.cpp:93-96, src/lsq.cpp:71-73).
+ * Here R comes from the Gram matrix; these entries expose the three device stages on host
+ * arrays (column-major complex128) so they can be checked on their own.
+ *
+ * mnb_chol_upper: in-place upper Cholesky G = R^H R of the Hermitian m x m matrix whose upper
+ * triangle is in G (the strictly lower triangle is zeroed); shift_factor * trace(G) is added to
+ * the diagonal first (0 = none).  status[6] = {info (LAPACK potrf convention), deficient (the rank
+ * rule of src/solver.cpp:25-33 with `rows` = rank_rows), min R_jj, max R_jj, trace(G), shift}.
+ * mnb_trtri_upper: X = R^{-1} for upper-triangular R; xnorm2 (optional) = ||X||_F^2.
+ * mnb_csne_solve: Step 2's z = Q R^{-H} b (src/solver.cpp:93-96) for the l x m sketch S from the
+ * corrected seminormal equations (Gram, Cholesky, inverse and refinement all on the device);
+ * status[4] = {accepted, corrections, ||b - S^H z||, ||z||}.                                   */
+int mnb_chol_upper(mnb_context* ctx, void* G, int64_t m, double shift_factor, double rank_rows, double* status);
+int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* xnorm2);
+int mnb_csne_solve(mnb_context* ctx, const void* S, int64_t l, int64_t m, const void* b, void* z, double* status);
+
 #ifdef __cplusplus
 }
 #endif

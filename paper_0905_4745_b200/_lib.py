@@ -79,7 +79,7 @@ EXPORTS = [
     "mnb_solve_least_squares",
     "mnb_srft_build", "mnb_srft_from_fields", "mnb_srft_destroy", "mnb_srft_get_field", "mnb_srft_dims",
     "mnb_srft_apply_h", "mnb_srft_apply", "mnb_srft_apply_adjoint", "mnb_srft_apply_to_columns", "mnb_dft",
-    "mnb_apply_adjoint_matrix", "mnb_bench_pcg_pass",
+    "mnb_apply_adjoint_matrix", "mnb_bench_pcg_pass", "mnb_chol_upper", "mnb_trtri_upper", "mnb_csne_solve",
 ]
 
 _lib = None
@@ -141,6 +141,9 @@ def load():
     L.mnb_srft_apply_to_columns.argtypes = [vp, vp, dp, ci]
     L.mnb_dft.argtypes = [vp, i64, dp, ci]
     L.mnb_bench_pcg_pass.argtypes = [vp, ci, ctypes.POINTER(ctypes.c_double)]
+    L.mnb_chol_upper.argtypes = [vp, dp, i64, ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+    L.mnb_trtri_upper.argtypes = [vp, dp, i64, dp, ctypes.POINTER(ctypes.c_double)]
+    L.mnb_csne_solve.argtypes = [vp, dp, i64, i64, dp, dp, ctypes.POINTER(ctypes.c_double)]
     _lib = L
     return L
 

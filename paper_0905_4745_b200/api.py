@@ -223,6 +223,35 @@ class Context:
         self.m, self.n, self.col_begin, self.n_local = m, n_global, col_begin, nl
         self.dtype = dtype
 
+    # ---- the sketch-QR building blocks (csrc/k_cholqr.cu), on host arrays
+    def chol_upper(self, G, shift_factor: float = 0.0, rank_rows: float = 0.0):
+        """Upper Cholesky R (G = R^H R) of a Hermitian matrix; returns (R, status dict)."""
+        G = np.array(G, dtype=np.complex128, order="F")
+        m = G.shape[0]
+        st = (ctypes.c_double * 6)()
+        _check(self._lib.mnb_chol_upper(self._h, _ptr(G), m, shift_factor, rank_rows, st))
+        return G, {"info": int(st[0]), "deficient": int(st[1]), "dmin": st[2], "dmax": st[3], "trace": st[4],
+                   "shift": st[5]}
+
+    def trtri_upper(self, R):
+        """Inverse of an upper-triangular matrix; returns (X, ||X||_F^2)."""
+        R = np.array(R, dtype=np.complex128, order="F")
+        m = R.shape[0]
+        X = np.empty((m, m), dtype=np.complex128, order="F")
+        xn = ctypes.c_double()
+        _check(self._lib.mnb_trtri_upper(self._h, _ptr(R), m, _ptr(X), ctypes.byref(xn)))
+        return X, xn.value
+
+    def csne_solve(self, S, b):
+        """Step 2's z = Q R^{-H} b (src/solver.cpp:93-96) of the sketch S = Q R; returns (z, status dict)."""
+        S = np.array(S, dtype=np.complex128, order="F")
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        l, m = S.shape
+        z = np.empty(l, dtype=np.complex128)
+        st = (ctypes.c_double * 4)()
+        _check(self._lib.mnb_csne_solve(self._h, _ptr(S), l, m, _ptr(b), _ptr(z), st))
+        return z, {"accepted": bool(st[0]), "corrections": int(st[1]), "residual": st[2], "znorm": st[3]}
+
     def bench_pcg_pass(self, reps: int = 10) -> float:
         out = ctypes.c_double()
         _check(self._lib.mnb_bench_pcg_pass(self._h, reps, ctypes.byref(out)))

@@ -62,6 +62,8 @@ void init_context(mnb::Context& c, int device) {
     if (const char* q = std::getenv("MNB_CSNE")) c.csne = std::string(q) != "0";
     if (const char* q = std::getenv("MNB_P2FA")) c.p2fa = std::string(q) != "0";
     if (const char* q = std::getenv("MNB_PRECOND_2NORM")) c.two_norm_check = std::string(q) != "0";
+    if (const char* q = std::getenv("MNB_FASTQR")) c.fastqr = std::string(q) != "0";
+    if (const char* q = std::getenv("MNB_QR_LIB")) c.qr_lib = std::string(q) == "1";
     if (cublasCreate(&c.cublas) != CUBLAS_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cublasCreate failed");
     cublasSetStream(c.cublas, c.stream);
     if (cusolverDnCreate(&c.cusolver) != CUSOLVER_STATUS_SUCCESS) throw mnb::Error(MNB_ERR_CUDA, "cusolverDnCreate failed");
@@ -80,6 +82,8 @@ std::unique_ptr<Context> make_helper_context(const Context& parent) {
     h->csne = parent.csne;
     h->p2fa = parent.p2fa;
     h->two_norm_check = parent.two_norm_check;
+    h->fastqr = parent.fastqr;
+    h->qr_lib = parent.qr_lib;
     return h;
 }
 }  // namespace mnb
@@ -519,6 +523,59 @@ int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch) {
         MNB_CUDA(cudaSetDevice(ctx->ctx.device));
         ctx->ctx.make_resident();
         *ms_per_launch = mnb::bench_pcg_pass(ctx->ctx, std::max(1, reps));
+    });
+}
+
+int mnb_chol_upper(mnb_context* ctx, void* G, int64_t m, double shift_factor, double rank_rows, double* status) {
+    return guard([&] {
+        auto& c = ctx->ctx;
+        mnb::require(m >= 1 && G && status, MNB_ERR_INVALID_ARGUMENT, "mnb_chol_upper: bad arguments");
+        MNB_CUDA(cudaSetDevice(c.device));
+        const size_t bytes = size_t(m) * size_t(m) * 16;
+        auto* Gd = static_cast<double2*>(c.gram.ensure(bytes));
+        auto* st = static_cast<mnb::CholStatus*>(c.qr_status.ensure(sizeof(mnb::CholStatus) + sizeof(mnb::RefineStatus)));
+        MNB_CUDA(cudaMemcpyAsync(Gd, G, bytes, cudaMemcpyHostToDevice, c.stream));
+        mnb::launch_chol_upper(Gd, m, m, shift_factor, rank_rows, st, c.num_sms, c.stream);
+        mnb::CholStatus h{};
+        MNB_CUDA(cudaMemcpyAsync(G, Gd, bytes, cudaMemcpyDeviceToHost, c.stream));
+        MNB_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        mnb::sync(c);
+        status[0] = h.info;
+        status[1] = h.deficient;
+        status[2] = h.dmin;
+        status[3] = h.dmax;
+        status[4] = h.trace;
+        status[5] = h.shift;
+    });
+}
+
+int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* xnorm2) {
+    return guard([&] {
+        auto& c = ctx->ctx;
+        mnb::require(m >= 1 && R && X, MNB_ERR_INVALID_ARGUMENT, "mnb_trtri_upper: bad arguments");
+        MNB_CUDA(cudaSetDevice(c.device));
+        const size_t bytes = size_t(m) * size_t(m) * 16;
+        auto* Rd = static_cast<double2*>(c.gram.ensure(bytes));
+        auto* Xd = static_cast<double2*>(c.Rinv.ensure(bytes));
+        auto* Wd = static_cast<double2*>(c.tri_work.ensure(bytes));
+        auto* st = static_cast<mnb::CholStatus*>(c.qr_status.ensure(sizeof(mnb::CholStatus) + sizeof(mnb::RefineStatus)));
+        MNB_CUDA(cudaMemcpyAsync(Rd, R, bytes, cudaMemcpyHostToDevice, c.stream));
+        mnb::launch_trtri_upper(Rd, m, m, Xd, Wd, st, c.num_sms, c.stream);
+        mnb::CholStatus h{};
+        MNB_CUDA(cudaMemcpyAsync(X, Xd, bytes, cudaMemcpyDeviceToHost, c.stream));
+        MNB_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+        mnb::sync(c);
+        if (xnorm2) *xnorm2 = h.xnorm2;
+    });
+}
+
+int mnb_csne_solve(mnb_context* ctx, const void* S, int64_t l, int64_t m, const void* b, void* z, double* status) {
+    return guard([&] {
+        auto& c = ctx->ctx;
+        mnb::require(m >= 1 && l >= m && S && b && z && status, MNB_ERR_INVALID_ARGUMENT, "mnb_csne_solve: bad arguments");
+        MNB_CUDA(cudaSetDevice(c.device));
+        mnb::csne_solve_host(c, static_cast<const double2*>(S), l, m, static_cast<const double2*>(b),
+                             static_cast<double2*>(z), status);
     });
 }
 

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "host_srft.hpp"
+#include "cholqr.cuh"
 #include "kernels.cuh"
 #include "pcg.cuh"
 
@@ -139,8 +140,15 @@ struct Context {
     bool two_norm_check = true;  // one-pass preconditioner accepted on a 2-norm cond estimate; MNB_PRECOND_2NORM=0 disables
     bool csne = true;    // Step 2 from R1 = chol(S^H S) + corrected seminormal equations; MNB_CSNE=0 disables
     bool cholqr = true;  // CholeskyQR2 for the sketch QRs (Householder fallback); MNB_QR=householder disables
+    // the sketch QRs on the hand-written kernels (k_cholqr.cu): Cholesky, triangular inverse and the
+    // device-resident Step-2 / preconditioner-check loops, one host read per sketch.
+    // MNB_FASTQR=0: the host-steered chain of cholqr_r; MNB_QR_LIB=1: cuSOLVER potrf + ZTRSM inverse
+    bool fastqr = true;
+    bool qr_lib = false;
+    DevBuf qr_status, qr_part, tri_work;
+    PinnedBuf pin_qr;
     DevBuf Rinv, Rinv_rows;
-    DevBuf vec_m[10], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;
+    DevBuf vec_m[12], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;
     DevBuf rhs, flag, out_c, qprobe;
     int* nonfinite = nullptr;  // set while sketching the problem matrix (finiteness check)
     PinnedBuf pin_params[2], pin_small;
@@ -213,5 +221,8 @@ void apply_adjoint_matrix(Context& ctx, const void* y, bool y_on_device, double2
 void solve_least_squares(Context& ctx, const double2* c_dev, const mnb_lsq_config& cfg, double2* y_host,
                          double* residual_norms, mnb_lsq_solution& sol);
 double bench_pcg_pass(Context& ctx, int reps);
+// Step 2 on a host sketch (mnb_csne_solve): Gram, Cholesky, inverse, corrected seminormal equations
+void csne_solve_host(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b, double2* z,
+                     double* status);
 
 }  // namespace mnb

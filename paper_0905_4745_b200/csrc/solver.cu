@@ -130,9 +130,15 @@ void fused_pass(Context& ctx, const PassBuffers& pb, int mode, const double2* w,
 }  // namespace
 
 // Rinv = R^{-1} for the upper-triangular m x m R (leading dimension ldR), the CG's explicit
-// preconditioner.  One tensor-core ZTRSM against the identity (MNB_TRTRI=1: cuSOLVER Xtrtri,
-// which measured ~2x slower at m = 2048); the strictly lower triangle of Rinv comes out zero.
-void upper_inverse(Context& ctx, const double2* R, int64_t ldR, int64_t m, double2* Rinv) {
+// preconditioner; the strictly lower triangle of Rinv comes out zero.  MNB_QR_LIB=1: one
+// tensor-core ZTRSM against the identity (or MNB_TRTRI=1: cuSOLVER Xtrtri, ~2x slower at m = 2048).
+void upper_inverse(Context& ctx, const double2* R, int64_t ldR, int64_t m, double2* Rinv, CholStatus* st = nullptr) {
+    if (!ctx.qr_lib) {  // the hand-written blocked inverse (k_cholqr.cu); st->xnorm2 = ||Rinv||_F^2
+        double2* W = dev<double2>(ctx.tri_work, size_t(m) * size_t(m));
+        launch_trtri_upper(R, ldR, m, Rinv, W, st, ctx.num_sms, ctx.stream, /*gate_on_chol=*/st != nullptr);
+        ctx.launches += 1;
+        return;
+    }
     static const bool use_trtri = [] { const char* e = std::getenv("MNB_TRTRI"); return e && std::string(e) == "1"; }();
     if (use_trtri) {
         MNB_CUDA(cudaMemcpy2DAsync(Rinv, size_t(m) * 16, R, size_t(ldR) * 16, size_t(m) * 16, size_t(m),
@@ -169,6 +175,41 @@ void trace(const char* what) {
 }
 
 void sync(Context& ctx) { MNB_CUDA(cudaStreamSynchronize(ctx.stream)); }
+
+// MNB_TRACE=1: device-side stage times of one stream (events between the stages; dump() waits
+// for the last one and prints the gaps).  Off: no events, no cost.
+struct DevTrace {
+    Context& ctx;
+    const char* what;
+    bool on;
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    DevTrace(Context& c, const char* w) : ctx(c), what(w), on(std::getenv("MNB_TRACE") != nullptr) { mark("start"); }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e;
+        MNB_CUDA(cudaEventCreate(&e));
+        MNB_CUDA(cudaEventRecord(e, ctx.stream));
+        marks.emplace_back(name, e);
+    }
+    void dump() {
+        if (!on || marks.empty()) return;
+        MNB_CUDA(cudaEventSynchronize(marks.back().second));
+        std::string line = std::string("[mnb] device ") + what + ":";
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].second, marks[i].second));
+            char buf[96];
+            std::snprintf(buf, sizeof buf, " %s %.3f", marks[i].first, ms);
+            line += buf;
+        }
+        std::fprintf(stderr, "%s ms\n", line.c_str());
+        for (auto& m : marks) cudaEventDestroy(m.second);
+        marks.clear();
+    }
+    ~DevTrace() {
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
+};
 
 Context::~Context() {
     for (auto e : events) if (e) cudaEventDestroy(e);
@@ -472,6 +513,7 @@ struct SketchQr {
     bool householder;
     int path = 0;       // 0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder, 3 one Cholesky pass (preconditioner)
     bool rinv_ready = false;  // path 3: R^{-1} already in ctx.Rinv
+    int64_t deficient = -1;   // the rank rule's count when the Cholesky kernel already took it (else -1)
 };
 
 // CholeskyQR2 of the l x m sketch, R only (S is left intact) -- or, for sketches too ill-
@@ -488,14 +530,52 @@ struct SketchQr {
 // to 1e-3 (cond(S) above ~2e6).  On success ctx.qwork holds Q1 and ctx.R2 holds R2.
 // r1_only: stop after the first Cholesky (R = R1, ctx.gram holds it too) -- Step 2's
 // corrected seminormal solve (step2_z_csne) needs nothing more.
+// One record per sketch QR on the device (and its pinned mirror): what the Cholesky, the inverse
+// and the refinement kernels found, read by the host once.
+struct QrStatus {
+    CholStatus chol;
+    RefineStatus ref;
+};
+QrStatus* qr_status_dev(Context& ctx) { return dev<QrStatus>(ctx.qr_status, 1); }
+const QrStatus& read_qr_status(Context& ctx) {
+    auto* h = static_cast<QrStatus*>(ctx.pin_qr.ensure(sizeof(QrStatus)));
+    MNB_CUDA(cudaMemcpyAsync(h, qr_status_dev(ctx), sizeof(QrStatus), cudaMemcpyDeviceToHost, ctx.stream));
+    MNB_CUDA(cudaStreamSynchronize(ctx.stream));
+    return *h;
+}
+// seeded dense start vector of the preconditioner check's power steps (splitmix64)
+void power_start_vector(std::vector<double2>& v0, int64_t m) {
+    v0.resize(size_t(m));
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    for (int64_t i = 0; i < m; ++i) {
+        auto nxt = [&h] {
+            uint64_t z = (h += 0x9E3779B97F4A7C15ull);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            return double((z ^ (z >> 31)) >> 11) * 0x1.0p-53 - 0.5;
+        };
+        v0[size_t(i)] = make_double2(nxt(), nxt());
+    }
+}
+// scratch of launch_sketch_refine: three m-vectors, the ||z||^2 partials
+void refine_scratch(Context& ctx, RefineArgs& a) {
+    a.v0 = dev<double2>(ctx.vec_m[8], size_t(a.m));
+    a.v1 = dev<double2>(ctx.vec_m[9], size_t(a.m));
+    a.v2 = dev<double2>(ctx.vec_m[10], size_t(a.m));
+    a.part = dev<double>(ctx.qr_part, size_t(a.l / 32 + 64));
+}
+
 bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted, bool* precond_only,
-              bool r1_only = false) {
+              bool r1_only = false, double rank_rows = 0.0, int64_t* deficient = nullptr) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* Q = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
     double2* Rp = dev<double2>(ctx.R2, size_t(m) * size_t(m));
     int* info = dev<int>(ctx.qr_info, 2);
+    QrStatus* qs = qr_status_dev(ctx);
     std::vector<double> diag(size_t(2 * m));
     int info_h = 0;
+    double dmin_h = 0.0, dmax_h = 0.0;
+    if (deficient) *deficient = -1;
     const double one = 1.0, zero = 0.0;
     const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0);
     auto herk = [&](const double2* X, double2* out) {
@@ -509,7 +589,26 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
                                    ctx.stream));
         MNB_CUDA(cudaStreamSynchronize(ctx.stream));
     };
-    auto potrf = [&](double2* A) {
+    // Upper Cholesky in place (+ a diagonal shift shift_factor * trace): the hand-written blocked
+    // kernel and one status read, or (MNB_QR_LIB=1) cuSOLVER Xpotrf steered from the host
+    auto potrf = [&](double2* A, double shift_factor) {
+        if (!ctx.qr_lib) {
+            launch_chol_upper(A, m, m, shift_factor, rank_rows, &qs->chol, ctx.num_sms, ctx.stream);
+            ctx.launches += 1;
+            const QrStatus& h = read_qr_status(ctx);
+            info_h = h.chol.info;
+            dmin_h = h.chol.dmin;
+            dmax_h = h.chol.dmax;
+            if (deficient && info_h == 0 && rank_rows > 0.0) *deficient = h.chol.deficient;
+            return;
+        }
+        if (shift_factor > 0.0) {
+            read_diag(A);
+            double tr = 0.0;
+            for (int64_t j = 0; j < m; ++j) tr += diag[size_t(2 * j)];
+            launch_add_diagonal(A, m, shift_factor * tr, ctx.stream);
+            ctx.launches += 1;
+        }
         size_t dws = 0, hws = 0;
         cusolver_check(cusolverDnXpotrf_bufferSize(ctx.cusolver, ctx.cusolver_params, CUBLAS_FILL_MODE_UPPER, m,
                                                    CUDA_C_64F, A, m, CUDA_C_64F, &dws, &hws),
@@ -523,6 +622,13 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         ctx.launches += 1;
         MNB_CUDA(cudaMemcpyAsync(&info_h, info, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
         read_diag(A);
+        dmax_h = 0.0;
+        dmin_h = 1e300;
+        for (int64_t j = 0; j < m; ++j) {
+            const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
+            dmax_h = std::max(dmax_h, a);
+            dmin_h = std::min(dmin_h, a);
+        }
     };
     auto trsm_q = [&](const double2* Rt) {  // Q <- Q Rt^{-1}
         cublas_check(cublasZtrsm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
@@ -531,45 +637,87 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
                                  reinterpret_cast<cuDoubleComplex*>(Q), int(l)),
                      "ztrsm");
     };
+    // the diagonal ratio of R1 bounds cond(S) from below: once u ratio^2 > 1e-3 neither a second
+    // Cholesky pass nor the seminormal corrections can reach orthogonality / the rounding floor
+    // (c3, kappa = 1e8): hand over to shifted CholeskyQR3 at once instead of failing later
+    auto ratio_bad = [&] { return !(dmin_h > 0.0) || kEps * (dmax_h / dmin_h) * (dmax_h / dmin_h) > 1e-3; };
+    DevTrace dt(ctx, shifted ? "cholqr (shifted)" : "cholqr");
+    struct DumpAtExit {
+        DevTrace& d;
+        ~DumpAtExit() {
+            try {
+                d.dump();
+            } catch (...) {
+            }
+        }
+    } dump_at_exit{dt};
     // pass 1: G = S^H S (+ shift) = R1^H R1, Q1 = S R1^{-1}  (or the Gram built during the sketch)
     if (ctx.pre_gram && !shifted)
         MNB_CUDA(cudaMemcpyAsync(G, ctx.pre_gram, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     else
         herk(S, G);
-    if (shifted) {
-        // shifted CholeskyQR (Fukaya et al.): s = 11 (l m + m (m + 1)) u ||S||^2, ||S||_2^2 <= trace(G)
-        read_diag(G);
-        double tr = 0.0;
-        for (int64_t j = 0; j < m; ++j) tr += diag[size_t(2 * j)];
-        const double shift = 11.0 * (double(l) * double(m) + double(m) * double(m + 1)) * kEps * tr;
-        launch_add_diagonal(G, m, shift, ctx.stream);
-        ctx.launches += 1;
-    }
-    potrf(G);
-    trace("  cholqr: gram + potrf");
-    if (info_h != 0) return false;
-    if (!shifted) {
-        double dmax = 0.0, dmin = 1e300;
-        for (int64_t j = 0; j < m; ++j) {
-            const double a = std::hypot(diag[size_t(2 * j)], diag[size_t(2 * j + 1)]);
-            dmax = std::max(dmax, a);
-            dmin = std::min(dmin, a);
+    dt.mark("gram");
+    // shifted CholeskyQR (Fukaya et al.): s = 11 (l m + m (m + 1)) u ||S||^2, ||S||_2^2 <= trace(G)
+    const double shift_factor = shifted ? 11.0 * (double(l) * double(m) + double(m) * double(m + 1)) * kEps : 0.0;
+    const bool fast_precond = !ctx.qr_lib && ctx.fastqr && !shifted && precond_only && *precond_only;
+    if (fast_precond) {
+        // The CG preconditioner needs only an R1 with Q1 = E R1^{-1} near-orthonormal (the CG rate and
+        // its stopping bound sigma_min(B R'^{-1}) >= 1, lsq.cpp:66-69, then move by < 1e-3): Cholesky,
+        // R1^{-1} (which the CG forms anyway, left in ctx.Rinv) and the check of ||Q1^H Q1 - I|| are
+        // three launches queued back to back; the host reads their verdict once.
+        double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
+        launch_chol_upper(G, m, m, 0.0, rank_rows, &qs->chol, ctx.num_sms, ctx.stream);
+        dt.mark("chol");
+        upper_inverse(ctx, G, m, m, Rinv, &qs->chol);
+        dt.mark("inverse");
+        RefineArgs ra;
+        ra.mode = REFINE_PRECOND;
+        ra.S = S;
+        ra.l = l;
+        ra.m = m;
+        ra.X = Rinv;
+        ra.chol = &qs->chol;
+        std::vector<double2> v0;
+        power_start_vector(v0, m);
+        double2* vstart = dev<double2>(ctx.vec_m[11], size_t(m));
+        MNB_CUDA(cudaMemcpyAsync(vstart, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+        ra.b = vstart;
+        ra.z = dev<double2>(ctx.qprobe, size_t(l));
+        refine_scratch(ctx, ra);
+        ra.st = &qs->ref;
+        ra.two_norm_check = ctx.two_norm_check ? 1 : 0;
+        launch_sketch_refine(ra, ctx.num_sms, ctx.stream);
+        dt.mark("check");
+        ctx.launches += 2;
+        const QrStatus& h = read_qr_status(ctx);
+        trace("  cholqr: gram + chol + R1^-1 + check (one read)");
+        info_h = h.chol.info;
+        dmin_h = h.chol.dmin;
+        dmax_h = h.chol.dmax;
+        if (info_h != 0 || ratio_bad()) return false;
+        if (deficient && rank_rows > 0.0) *deficient = h.chol.deficient;
+        if (std::getenv("MNB_TRACE"))
+            std::fprintf(stderr, "[mnb] one-pass preconditioner: u cond^2 <= %.2e (Frobenius), ||Q1^H Q1 - I|| ~ %.2e (%d steps)\n",
+                         h.ref.thr, h.ref.best, h.ref.iterations);
+        if (h.ref.accepted) {
+            MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+            return true;
         }
-        // the diagonal ratio of R1 bounds cond(S) from below: once u ratio^2 > 1e-3 neither a second
-        // Cholesky pass nor the seminormal corrections can reach orthogonality / the rounding floor
-        // (c3, kappa = 1e8): hand over to shifted CholeskyQR3 at once instead of failing later
-        if (!(dmin > 0.0) || kEps * (dmax / dmin) * (dmax / dmin) > 1e-3) return false;
+        *precond_only = false;  // R'^{-1} in ctx.Rinv is stale: the full factorization follows from R1
+    } else {
+        potrf(G, shift_factor);
+        dt.mark("chol");
+        trace("  cholqr: gram + potrf");
+        if (info_h != 0) return false;
+        if (!shifted && ratio_bad()) return false;
     }
     if (r1_only) {
         MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
         return true;
     }
     if (precond_only && *precond_only) {
-        // The CG preconditioner needs only an R1 with E R1^{-1} near-orthonormal -- and
-        // |Q1^H Q1 - I| ~ u cond(E)^2 <= u ||R1||_F^2 ||R1^{-1}||_F^2.  When that bound is below
-        // 1e-3 one Cholesky pass is enough (the CG rate and its stopping bound sigma_min(B R'^{-1})
-        // >= 1, lsq.cpp:66-69, move by < 1e-3): no Q1, no second pass, and R'^{-1} (which the CG
-        // forms anyway) is left in ctx.Rinv.
+        // (MNB_FASTQR=0 / MNB_QR_LIB=1: the same acceptance steered from the host)  The bound
+        // |Q1^H Q1 - I| ~ u cond(E)^2 <= u ||R1||_F^2 ||R1^{-1}||_F^2 first.
         double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
         upper_inverse(ctx, G, m, m, Rinv);
         double nr = 0.0, nri = 0.0;  // lower triangles are zero
@@ -594,17 +742,8 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             const auto* Sc = reinterpret_cast<const cuDoubleComplex*>(S);
             const auto* Ri = reinterpret_cast<const cuDoubleComplex*>(Rinv);
             const cuDoubleComplex czero = make_cuDoubleComplex(0.0, 0.0);
-            std::vector<double2> v0(static_cast<size_t>(m));
-            uint64_t h = 0x9E3779B97F4A7C15ull;
-            for (int64_t i = 0; i < m; ++i) {  // seeded pseudo-random start (splitmix64)
-                auto nxt = [&h] {
-                    uint64_t z = (h += 0x9E3779B97F4A7C15ull);
-                    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-                    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-                    return double((z ^ (z >> 31)) >> 11) * 0x1.0p-53 - 0.5;
-                };
-                v0[size_t(i)] = make_double2(nxt(), nxt());
-            }
+            std::vector<double2> v0;
+            power_start_vector(v0, m);
             MNB_CUDA(cudaMemcpyAsync(v, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
             // device pointer mode: the ten steps run without a host round trip; one read at the end
             double* nrm_d = dev<double>(ctx.scratch, 512);
@@ -615,7 +754,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             cublas_check(cublasDznrm2(ctx.cublas, int(m), vc, 1, nrm_d), "dznrm2");
             for (int it = 0; it < 10; ++it) {
                 launch_unit_copy(v, a, m, nrm_d, ctx.stream);                    // v = v / ||v||, a = v
-                // (R1^{-1} from ZTRSM against I: its strict lower triangle is exactly zero, so a plain
+                // (R1^{-1}: its strict lower triangle is exactly zero, so a plain
                 // GEMV -- one streaming read, no triangular dependency chain -- applies it)
                 cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(m), int(m), consts, Ri, int(m), vc, 1, consts + 1,
                                          ac, 1), "zgemv");                      // a = R1^{-1} v
@@ -648,11 +787,13 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
     MNB_CUDA(cudaMemcpyAsync(Q, S, size_t(l) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     trsm_q(G);
     MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+    dt.mark("Q1 = S R1^-1");
     // passes 2 (and 3): R_p = chol(Q^H Q); R <- R_p R; on the last pass Q must already be
     // orthonormal to 1e-3 (|Q^H Q - I| ~ eps cond^2) for R to be accurate -- else Householder.
     const int passes = shifted ? 3 : 2;
     for (int p = 2; p <= passes; ++p) {
         herk(Q, Rp);
+        dt.mark("gram");
         if (p == passes) {
             double* dev_max = dev<double>(ctx.scratch, 512);
             launch_max_offset_from_identity(Rp, m, dev_max, ctx.stream);
@@ -662,15 +803,21 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             MNB_CUDA(cudaStreamSynchronize(ctx.stream));
             if (!(gmax < 1e-3)) return false;
         }
-        potrf(Rp);
+        potrf(Rp, 0.0);
+        dt.mark("chol");
         if (info_h != 0) return false;
-        if (p < passes) trsm_q(Rp);
+        if (p < passes) {
+            trsm_q(Rp);
+            dt.mark("Q = Q Rp^-1");
+        }
         cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
                                  CUBLAS_DIAG_NON_UNIT, int(m), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(Rp),
                                  int(m), reinterpret_cast<const cuDoubleComplex*>(R), int(m),
                                  reinterpret_cast<cuDoubleComplex*>(R), int(m)),
                      "ztrmm");
+        dt.mark("R = Rp R");
     }
+    if (deficient) *deficient = -1;  // the rank rule applies to the final R: the caller reads its diagonal
     return true;  // ctx.qwork holds Q_{passes-1}, ctx.R2 the last R_p:  Q = Q_{passes-1} R_p^{-1}
 }
 
@@ -678,8 +825,9 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
 // precond: the preconditioner's QR (E), which may stop after one Cholesky pass (path 3).
 // seminormal: Step 2's QR (S), which may stop after R1 = chol(S^H S) (path 4) -- step2_z_csne
 // then solves with the corrected seminormal equations and falls back here if they do not converge.
+// rank_rows: the `rows` of the rank rule the caller will apply (lets the Cholesky kernel take it).
 SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBuf& Rbuf, double* qr_s,
-                      bool precond = false, bool seminormal = false) {
+                      bool precond = false, bool seminormal = false, double rank_rows = 0.0) {
     const int64_t m = ctx.m;
     double2* tau = dev<double2>(taubuf, size_t(m));
     double2* R = dev<double2>(Rbuf, size_t(m) * size_t(m));
@@ -691,14 +839,14 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
     // this solve needed it, the next one starts there); Householder (the reference's) as the last resort
     bool done = false;
     if (ctx.cholqr && seminormal && ctx.csne && !ctx.qr_shifted) {
-        done = cholqr_r(ctx, S, l, m, R, false, nullptr, /*r1_only=*/true);
+        done = cholqr_r(ctx, S, l, m, R, false, nullptr, /*r1_only=*/true, rank_rows, &out.deficient);
         if (done) out.path = 4;
         else ctx.qr_shifted = true;  // the first Cholesky pass failed: CholeskyQR2 would too
     }
     if (ctx.cholqr && !done) {
         if (!ctx.qr_shifted) {
             bool one_pass = precond;
-            done = cholqr_r(ctx, S, l, m, R, false, &one_pass);
+            done = cholqr_r(ctx, S, l, m, R, false, &one_pass, false, rank_rows, &out.deficient);
             if (done && one_pass) {
                 out.path = 3;
                 out.rinv_ready = true;
@@ -869,6 +1017,59 @@ bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const doub
         cublas_check(cublasZgemv(ctx.cublas, CUBLAS_OP_N, int(l), int(m), &one, Sc, int(l), wc, 1, &one, zc, 1), "zgemv");
     }
     return best <= thr * nz_best;
+}
+
+// QR(S) and Step 2 (src/solver.cpp:85-97) queued on ctx.stream without a host round trip:
+// G = S^H S (cuBLAS ZHERK, a plain library GEMM), R1 = chol(G) with the rank rule taken on its
+// diagonal, X = R1^{-1}, then the corrected seminormal equations of step2_z_csne as one
+// persistent kernel; their findings land in the context's QrStatus record.
+void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b_host, double2* z,
+                       DevTrace* dt = nullptr) {
+    double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
+    double2* X = dev<double2>(ctx.R2, size_t(m) * size_t(m));
+    QrStatus* qs = qr_status_dev(ctx);
+    const double one = 1.0, zero = 0.0;
+    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
+                             reinterpret_cast<const cuDoubleComplex*>(S), int(l), &zero,
+                             reinterpret_cast<cuDoubleComplex*>(G), int(m)),
+                 "zherk");
+    if (dt) dt->mark("gram");
+    launch_chol_upper(G, m, m, 0.0, double(l), &qs->chol, ctx.num_sms, ctx.stream);
+    if (dt) dt->mark("chol");
+    upper_inverse(ctx, G, m, m, X, &qs->chol);
+    if (dt) dt->mark("inverse");
+    double2* bd = dev<double2>(ctx.vec_m[6], size_t(m));
+    MNB_CUDA(cudaMemcpyAsync(bd, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    RefineArgs ra;
+    ra.mode = REFINE_CSNE;
+    ra.S = S;
+    ra.l = l;
+    ra.m = m;
+    ra.X = X;
+    ra.chol = &qs->chol;
+    ra.b = bd;
+    ra.z = z;
+    refine_scratch(ctx, ra);
+    ra.st = &qs->ref;
+    launch_sketch_refine(ra, ctx.num_sms, ctx.stream);
+    if (dt) dt->mark("csne");
+    ctx.launches += 2;
+}
+
+void csne_solve_host(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b, double2* z,
+                     double* status) {
+    double2* Sd = dev<double2>(ctx.sk_S, size_t(l) * size_t(m));
+    double2* zd = dev<double2>(ctx.rhs, size_t(l));
+    MNB_CUDA(cudaMemcpyAsync(Sd, S, size_t(l) * size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    cublasSetStream(ctx.cublas, ctx.stream);
+    launch_fast_step2(ctx, Sd, l, m, b, zd);
+    const QrStatus h = read_qr_status(ctx);
+    MNB_CUDA(cudaMemcpyAsync(z, zd, size_t(l) * 16, cudaMemcpyDeviceToHost, ctx.stream));
+    sync(ctx);
+    status[0] = (h.chol.info == 0 && h.ref.accepted) ? 1.0 : 0.0;
+    status[1] = h.ref.iterations;
+    status[2] = h.ref.best;
+    status[3] = h.ref.nz_best;
 }
 
 // ---------------------------------------------------- solve_randomized ----
@@ -1121,8 +1322,8 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             PreGram(Context& c, const double2* g) : q(c) { q.pre_gram = g; }
             ~PreGram() { q.pre_gram = nullptr; }
         } pre_gram{q, GE};
-        eq = qr_of_sketch(q, Ebuf, l, q.tau_E, q.R_E, &qr_s1, /*precond=*/true);
-        if (int64_t bad = deficient_count(q, eq.R, eq.ldR, m, n); bad > 0)
+        eq = qr_of_sketch(q, Ebuf, l, q.tau_E, q.R_E, &qr_s1, /*precond=*/true, false, double(n));
+        if (int64_t bad = eq.deficient >= 0 ? eq.deficient : deficient_count(q, eq.R, eq.ldR, m, n); bad > 0)
             throw Error(MNB_ERR_RANK_DEFICIENCY,
                         "solve_least_squares: sketch QR found " + std::to_string(bad) +
                             " numerically dependent columns",
@@ -1149,6 +1350,52 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     {
         OnStream on(ctx, s2);
         MNB_CUDA(cudaStreamWaitEvent(s2, eS, 0));
+        // QR(S), Step 2 and Step 3 queued back to back on the hand-written kernels (Gram, Cholesky,
+        // R1^{-1}, the corrected-seminormal loop, T^* z): the host reads their verdict once.  When the
+        // sketch is too ill-conditioned for one Cholesky pass (pivot failure, diagonal ratio, the
+        // corrections stall above the rounding level) the host-steered chain below takes over,
+        // starting at shifted CholeskyQR3 -- exactly where it would have ended up.
+        bool fast_done = false;
+        if (ctx.fastqr && !ctx.qr_lib && ctx.cholqr && ctx.csne && !ctx.qr_shifted) {
+            cudaEvent_t q1 = ctx.timer_event(), q2 = ctx.timer_event();
+            MNB_CUDA(cudaEventRecord(q1, ctx.stream));
+            DevTrace dt(ctx, "QR(S) + steps 2-3");
+            launch_fast_step2(ctx, Sbuf, l, m, b_host, z, &dt);
+            MNB_CUDA(cudaEventRecord(q2, ctx.stream));
+            srft_adjoint_vec(ctx, Td, z, c_vec);
+            dt.mark("T^* z");
+            MNB_CUDA(cudaEventRecord(eC, ctx.stream));
+            int* flag_h = static_cast<int*>(ctx.pin_small.ensure(sizeof(CgState) + 64)) + (sizeof(CgState) + 32) / 4;
+            MNB_CUDA(cudaMemcpyAsync(flag_h, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+            const QrStatus& h = read_qr_status(ctx);
+            trace("QR(S) + steps 2-3 (one read)");
+            dt.dump();
+            if (*flag_h) throw Error(MNB_ERR_DIMENSION, "matrix and right-hand side entries must be finite");
+            float qms = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&qms, q1, q2));
+            qr_s0 += qms * 1e-3;
+            const double ratio = h.chol.dmin > 0.0 ? h.chol.dmax / h.chol.dmin : 1e300;
+            if (h.chol.info == 0 && !(kEps * ratio * ratio > 1e-3)) {
+                if (h.chol.deficient > 0)
+                    throw Error(MNB_ERR_RANK_DEFICIENCY,
+                                "sketch S = T A* lost rank (" + std::to_string(h.chol.deficient) +
+                                    " dependent columns); the problem matrix is rank deficient",
+                                h.chol.deficient);
+                fast_done = h.ref.accepted != 0;
+            }
+            if (std::getenv("MNB_TRACE"))
+                std::fprintf(stderr, "[mnb] fast QR(S): info %d, diag ratio %.2e, csne %d corrections, ||b - S^H z|| %.3e (thr %.3e) -> %s\n",
+                             h.chol.info, ratio, h.ref.iterations, h.ref.best, h.ref.thr * h.ref.nz_best,
+                             fast_done ? "accepted" : "fallback");
+            if (fast_done) {
+                sq = SketchQr{Sbuf, nullptr, ctx.gram.as<double2>(), m, false};
+                sq.path = 4;
+                rep.step_seconds[0] = now_s() - t0;
+            } else {
+                ctx.qr_shifted = true;
+            }
+        }
+        if (!fast_done) {
         sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0, false, /*seminormal=*/true);
     trace("QR(S)");
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
@@ -1183,6 +1430,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         MNB_CUDA(cudaEventRecord(eC, ctx.stream));
         sync(ctx);
         rep.step_seconds[2] = now_s() - t0;
+        }
     }
     trace("steps 2-3");
     const double2* c_loc = c_vec + ctx.col_begin;

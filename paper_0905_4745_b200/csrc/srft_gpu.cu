@@ -403,7 +403,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
         // keep room for what the solve allocates after the first sketch: the second
         // sketch E (l x m), the CholeskyQR2 copy (l x m), R, R', Gram, R'^{-1} twice (m x m), the second operator
         const size_t mm = size_t(ctx.m), ll = size_t(h.l);
-        const size_t reserve = (size_t(2) << 30) + 40 * ll * mm + 96 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
+        const size_t reserve = (size_t(2) << 30) + 40 * ll * mm + 128 * mm * mm + 2 * (h.device_bytes + 96 * size_t(n));
         const size_t budget = have > 2 * reserve ? have - reserve : have / 2;
         int64_t ms = std::min<int64_t>(rows, int64_t(budget / (size_t(32) * size_t(n))));
         if (ms < rows) ms = std::max<int64_t>(8, ms & ~int64_t(7));

@@ -137,7 +137,9 @@ typedef struct {
     int32_t qr_path;         /* extension: sketch QR used, S in bits 0-3, E in bits 4-7:
                                 0 CholeskyQR2, 1 shifted CholeskyQR3, 2 Householder,
                                 3 one Cholesky pass (E, preconditioner only),
-                                4 one Cholesky pass + corrected seminormal Step 2 (S)  */
+                                4 one Cholesky pass + corrected seminormal Step 2 (S),
+                                5 shifted two-pass Cholesky (E, preconditioner only),
+                                6 shifted two-pass Cholesky + corrected seminormal Step 2 (S) */
     int64_t sketch_size;     /* SolveReport::sketch_size                                */
     double lsq_tau;          /* SolveReport::lsq_tau                                    */
     /* ---- extensions (not in the reference report) ---- */
@@ -271,14 +273,15 @@ int mnb_bench_pcg_pass(mnb_context* ctx, int reps, double* ms_per_launch);
  *
  * mnb_chol_upper: in-place upper Cholesky G = R^H R of the Hermitian m x m matrix whose upper
  * triangle is in G (the strictly lower triangle is zeroed); shift_factor * trace(G) is added to
- * the diagonal first (0 = none).  status[6] = {info (LAPACK potrf convention), deficient (the rank
- * rule of src/solver.cpp:25-33 with `rows` = rank_rows), min R_jj, max R_jj, trace(G), shift}.
- * mnb_trtri_upper: X = R^{-1} for upper-triangular R; xnorm2 (optional) = ||X||_F^2.
+ * the diagonal first (0 = none).  status[7] = {info (LAPACK potrf convention), deficient (the rank
+ * rule of src/solver.cpp:25-33 with `rows` = rank_rows), min R_jj, max R_jj, trace(G), shift,
+ * kernel milliseconds (CUDA events)}.
+ * mnb_trtri_upper: X = R^{-1} for upper-triangular R; out2 (optional) = {||X||_F^2, kernel ms}.
  * mnb_csne_solve: Step 2's z = Q R^{-H} b (src/solver.cpp:93-96) for the l x m sketch S from the
  * corrected seminormal equations (Gram, Cholesky, inverse and refinement all on the device);
  * status[4] = {accepted, corrections, ||b - S^H z||, ||z||}.                                   */
 int mnb_chol_upper(mnb_context* ctx, void* G, int64_t m, double shift_factor, double rank_rows, double* status);
-int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* xnorm2);
+int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* out2);
 int mnb_csne_solve(mnb_context* ctx, const void* S, int64_t l, int64_t m, const void* b, void* z, double* status);
 
 #ifdef __cplusplus

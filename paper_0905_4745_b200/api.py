@@ -228,19 +228,20 @@ class Context:
         """Upper Cholesky R (G = R^H R) of a Hermitian matrix; returns (R, status dict)."""
         G = np.array(G, dtype=np.complex128, order="F")
         m = G.shape[0]
-        st = (ctypes.c_double * 6)()
+        st = (ctypes.c_double * 7)()
         _check(self._lib.mnb_chol_upper(self._h, _ptr(G), m, shift_factor, rank_rows, st))
         return G, {"info": int(st[0]), "deficient": int(st[1]), "dmin": st[2], "dmax": st[3], "trace": st[4],
-                   "shift": st[5]}
+                   "shift": st[5], "kernel_ms": st[6]}
 
     def trtri_upper(self, R):
         """Inverse of an upper-triangular matrix; returns (X, ||X||_F^2)."""
         R = np.array(R, dtype=np.complex128, order="F")
         m = R.shape[0]
         X = np.empty((m, m), dtype=np.complex128, order="F")
-        xn = ctypes.c_double()
-        _check(self._lib.mnb_trtri_upper(self._h, _ptr(R), m, _ptr(X), ctypes.byref(xn)))
-        return X, xn.value
+        out = (ctypes.c_double * 2)()
+        _check(self._lib.mnb_trtri_upper(self._h, _ptr(R), m, _ptr(X), out))
+        self.last_kernel_ms = out[1]
+        return X, out[0]
 
     def csne_solve(self, S, b):
         """Step 2's z = Q R^{-H} b (src/solver.cpp:93-96) of the sketch S = Q R; returns (z, status dict)."""

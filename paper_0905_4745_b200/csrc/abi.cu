@@ -535,7 +535,9 @@ int mnb_chol_upper(mnb_context* ctx, void* G, int64_t m, double shift_factor, do
         auto* Gd = static_cast<double2*>(c.gram.ensure(bytes));
         auto* st = static_cast<mnb::CholStatus*>(c.qr_status.ensure(sizeof(mnb::CholStatus) + sizeof(mnb::RefineStatus)));
         MNB_CUDA(cudaMemcpyAsync(Gd, G, bytes, cudaMemcpyHostToDevice, c.stream));
+        MNB_CUDA(cudaEventRecord(c.event(60), c.stream));
         mnb::launch_chol_upper(Gd, m, m, shift_factor, rank_rows, st, c.num_sms, c.stream);
+        MNB_CUDA(cudaEventRecord(c.event(61), c.stream));
         mnb::CholStatus h{};
         MNB_CUDA(cudaMemcpyAsync(G, Gd, bytes, cudaMemcpyDeviceToHost, c.stream));
         MNB_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
@@ -546,10 +548,13 @@ int mnb_chol_upper(mnb_context* ctx, void* G, int64_t m, double shift_factor, do
         status[3] = h.dmax;
         status[4] = h.trace;
         status[5] = h.shift;
+        float ms = 0.f;
+        MNB_CUDA(cudaEventElapsedTime(&ms, c.event(60), c.event(61)));
+        status[6] = ms;
     });
 }
 
-int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* xnorm2) {
+int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double* xnorm2) {  // xnorm2: out2
     return guard([&] {
         auto& c = ctx->ctx;
         mnb::require(m >= 1 && R && X, MNB_ERR_INVALID_ARGUMENT, "mnb_trtri_upper: bad arguments");
@@ -560,12 +565,19 @@ int mnb_trtri_upper(mnb_context* ctx, const void* R, int64_t m, void* X, double*
         auto* Wd = static_cast<double2*>(c.tri_work.ensure(bytes));
         auto* st = static_cast<mnb::CholStatus*>(c.qr_status.ensure(sizeof(mnb::CholStatus) + sizeof(mnb::RefineStatus)));
         MNB_CUDA(cudaMemcpyAsync(Rd, R, bytes, cudaMemcpyHostToDevice, c.stream));
+        MNB_CUDA(cudaEventRecord(c.event(60), c.stream));
         mnb::launch_trtri_upper(Rd, m, m, Xd, Wd, st, c.num_sms, c.stream);
+        MNB_CUDA(cudaEventRecord(c.event(61), c.stream));
         mnb::CholStatus h{};
         MNB_CUDA(cudaMemcpyAsync(X, Xd, bytes, cudaMemcpyDeviceToHost, c.stream));
         MNB_CUDA(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c.stream));
         mnb::sync(c);
-        if (xnorm2) *xnorm2 = h.xnorm2;
+        if (xnorm2) {
+            xnorm2[0] = h.xnorm2;
+            float ms = 0.f;
+            MNB_CUDA(cudaEventElapsedTime(&ms, c.event(60), c.event(61)));
+            xnorm2[1] = ms;
+        }
     });
 }
 

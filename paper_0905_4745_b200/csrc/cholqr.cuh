@@ -50,6 +50,10 @@ void launch_chol_upper(double2* G, int64_t m, int64_t ld, double shift_factor, d
 void launch_trtri_upper(const double2* R, int64_t ldr, int64_t m, double2* X, double2* W, CholStatus* st,
                         int num_sms, cudaStream_t stream, bool gate_on_chol = false);
 
+// st->deficient = the rank rule's count on the diagonal of R = R2 R1 (two upper Cholesky factors)
+void launch_diag_product_rank(const double2* R2, int64_t ld2, const double2* R1, int64_t ld1, int64_t m, double rows,
+                              CholStatus* st, cudaStream_t stream);
+
 enum RefineMode { REFINE_CSNE = 0, REFINE_PRECOND = 1 };
 struct RefineArgs {
     int mode = REFINE_CSNE;

@@ -145,7 +145,8 @@ struct Context {
     // MNB_FASTQR=0: the host-steered chain of cholqr_r; MNB_QR_LIB=1: cuSOLVER potrf + ZTRSM inverse
     bool fastqr = true;
     bool qr_lib = false;
-    DevBuf qr_status, qr_part, tri_work;
+    DevBuf qr_status, qr_part, tri_work, tri_x1;
+    const double2* gram0 = nullptr;  // this sketch's Gram S^H S kept beside the one-pass Cholesky (shifted two-pass chain)
     PinnedBuf pin_qr;
     DevBuf Rinv, Rinv_rows;
     DevBuf vec_m[12], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;

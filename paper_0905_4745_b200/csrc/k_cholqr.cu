@@ -147,12 +147,12 @@ __global__ void __launch_bounds__(TH, 1)
 chol_upper_kernel(double2* G, int64_t m, int64_t ld, double shift_factor, double rank_rows, CholStatus* st) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double2 smem[];
-    double2* D = smem;              // [NB][LDD] the diagonal block / its factor
-    double2* As = D + NB * LDD;     // [KC][LDT]
+    double2* W = smem;              // [NB][LDD] the diagonal block while it is eliminated
+    double2* As = W + NB * LDD;     // [KC][LDT]
     double2* Bs = As + KC * LDT;    // [KC][LDT]
+    double2* D = Bs + KC * LDT;     // [NB][LDD] its factor R_kk
     __shared__ double red[NW];
     __shared__ double rdiag[NB];
-    __shared__ double2 rowbuf[NB];
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int ng = gridDim.x, c = blockIdx.x;
 
@@ -174,33 +174,35 @@ chol_upper_kernel(double2* G, int64_t m, int64_t ld, double shift_factor, double
                 v = __ldcg(G + (k0 + i) + (k0 + j) * ld);
                 if (i == j) v = make_double2(v.x + shift, 0.0);
             }
-            D[i * LDD + j] = v;
+            W[i * LDD + j] = v;
+            D[i * LDD + j] = make_double2(0.0, 0.0);
         }
+        // one barrier per pivot: row j of W is final when step j starts and is only read in it
+        // (the scaled row goes to D, the rows below take the rank-1 update with 1 / pivot)
         for (int j = 0; j < nb; ++j) {
             __syncthreads();
-            const double piv = D[j * LDD + j].x;
+            const double piv = W[j * LDD + j].x;
             if (!(piv > 0.0) || !(piv < 1e300)) {  // not positive definite (or not finite): potrf's info
                 info = int(k0) + j + 1;
                 break;
             }
-            const double r = sqrt(piv), rinv = 1.0 / r;
-            if (t < NB) {  // row j of R
-                const double2 v = D[j * LDD + t];
-                rowbuf[t] = t > j ? make_double2(v.x * rinv, v.y * rinv)
-                                  : (t == j ? make_double2(r, 0.0) : make_double2(0.0, 0.0));
-                if (t == j) rdiag[j] = rinv;
-            }
-            __syncthreads();
+            const double rinv = rsqrt(piv), r = piv * rinv, pinv = rinv * rinv;
+            if (t == 0) rdiag[j] = rinv;
             const int cc = t % NB;
             for (int i = t / NB; i < nb; i += TH / NB) {
                 if (i == j) {
-                    if (cc >= j) D[j * LDD + cc] = rowbuf[cc];
+                    if (cc > j && cc < nb) {
+                        const double2 v = W[j * LDD + cc];
+                        D[j * LDD + cc] = make_double2(v.x * rinv, v.y * rinv);
+                    } else if (cc == j) {
+                        D[j * LDD + j] = make_double2(r, 0.0);
+                    }
                 } else if (i > j && cc >= i && cc < nb) {
-                    const double2 a = rowbuf[i], b = rowbuf[cc];
-                    double2 d = D[i * LDD + cc];
-                    d.x -= fma(a.x, b.x, a.y * b.y);   // conj(a) b
-                    d.y -= fma(a.x, b.y, -a.y * b.x);
-                    D[i * LDD + cc] = d;
+                    const double2 a = W[j * LDD + i], b = W[j * LDD + cc];
+                    double2 d = W[i * LDD + cc];
+                    d.x = fma(-pinv, fma(a.x, b.x, a.y * b.y), d.x);   // conj(a) b / pivot
+                    d.y = fma(-pinv, fma(a.x, b.y, -a.y * b.x), d.y);
+                    W[i * LDD + cc] = d;
                 }
             }
             dmin = fmin(dmin, r);
@@ -630,23 +632,52 @@ __global__ void __launch_bounds__(TH, 1) sketch_refine_kernel(const RefineArgs p
     }
 }
 
+// Rank rule (src/solver.cpp:25-33, src/lsq.cpp:18-27) on the diagonal of R = R2 R1 (both upper
+// triangular with positive diagonals, so R_jj = R2_jj R1_jj): st->deficient.  One CTA.
+__global__ void __launch_bounds__(TH, 1)
+diag_product_rank_kernel(const double2* R2, int64_t ld2, const double2* R1, int64_t ld1, int64_t m, double rows,
+                         CholStatus* st) {
+    __shared__ double red[NW];
+    double dmax = 0.0;
+    for (int64_t j = threadIdx.x; j < m; j += TH)
+        dmax = fmax(dmax, fabs(__ldcg(R2 + j + j * ld2).x) * fabs(__ldcg(R1 + j + j * ld1).x));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dmax;
+    __syncthreads();
+    dmax = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) dmax = fmax(dmax, red[q]);
+    const double thr = rows * kU * dmax;
+    double bad = 0.0;
+    for (int64_t j = threadIdx.x; j < m; j += TH) {
+        const double d = fabs(__ldcg(R2 + j + j * ld2).x) * fabs(__ldcg(R1 + j + j * ld1).x);
+        if (d < thr || d == 0.0) bad += 1.0;
+    }
+    bad = block_sum(bad, red);
+    if (threadIdx.x == 0) st->deficient = int(bad);
+}
+
 constexpr size_t kTileSmem = size_t(NB * LDD + 2 * KC * LDT) * sizeof(double2);
+constexpr size_t kCholSmem = kTileSmem + size_t(NB * LDD) * sizeof(double2);
 
 }  // namespace
 
 int chol_grid(int64_t m, int num_sms) {
     const int64_t nt = (std::max<int64_t>(m - NB, 0) + TB - 1) / TB;
     const int64_t tiles = nt * (nt + 1) / 2;
-    return int(std::max<int64_t>(1, std::min<int64_t>(num_sms, std::max<int64_t>(tiles, (m + TB - 1) / TB))));
+    // enough CTAs for the first trailing update's tiles and for one panel column per warp
+    const int64_t panel = (std::max<int64_t>(m - NB, 0) + NW - 1) / NW;
+    return int(std::max<int64_t>(1, std::min<int64_t>(num_sms, std::max<int64_t>(tiles, panel))));
 }
 
 void launch_chol_upper(double2* G, int64_t m, int64_t ld, double shift_factor, double rank_rows, CholStatus* st,
                        int num_sms, cudaStream_t stream) {
     auto k = chol_upper_kernel;
-    MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTileSmem)));
+    MNB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCholSmem)));
     void* params[] = {&G, &m, &ld, &shift_factor, &rank_rows, &st};
     MNB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(chol_grid(m, num_sms)), dim3(TH),
-                                         params, kTileSmem, stream));
+                                         params, kCholSmem, stream));
 }
 
 void launch_trtri_upper(const double2* R, int64_t ldr, int64_t m, double2* X, double2* W, CholStatus* st,
@@ -662,6 +693,12 @@ void launch_trtri_upper(const double2* R, int64_t ldr, int64_t m, double2* X, do
     void* params[] = {&R, &ldr, &m, &X, &W, &st, &part, &gate};
     MNB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(TH), params, kTileSmem,
                                          stream));
+}
+
+void launch_diag_product_rank(const double2* R2, int64_t ld2, const double2* R1, int64_t ld1, int64_t m, double rows,
+                              CholStatus* st, cudaStream_t stream) {
+    diag_product_rank_kernel<<<1, TH, 0, stream>>>(R2, ld2, R1, ld1, m, rows, st);
+    MNB_LAUNCH_CHECK();
 }
 
 void launch_sketch_refine(const RefineArgs& a, int num_sms, cudaStream_t stream) {

@@ -88,15 +88,29 @@ __global__ void __launch_bounds__(kThreads) hstage_kernel(Fetch f, Emit e, const
         double2 carry = f.load(r, f.src_of(start));
         const int64_t lo = i0 > 0 ? i0 - 1 : 0;
         int64_t j = start - 1;
-        while (j >= lo) {
+        // two batches in flight: the next batch's (index -> element) loads are issued before the
+        // current batch's dependent recurrence runs (a single row is pure load latency otherwise)
+        double2 x[kUnroll], cs[kUnroll], xn[kUnroll], csn[kUnroll];
+        int cnt = 0;
+        {
             const int64_t left = j - lo + 1;
-            const int cnt = int(left < kUnroll ? left : kUnroll);
-            double2 x[kUnroll], cs[kUnroll];
+            cnt = int(left < kUnroll ? (left > 0 ? left : 0) : kUnroll);
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
                 if (u < cnt) {
                     x[u] = f.load(r, f.src_of(j - u));
                     cs[u] = __ldg(cssn + (j - u));
+                }
+        }
+        while (cnt > 0) {
+            const int64_t jn = j - cnt;
+            const int64_t leftn = jn - lo + 1;
+            const int cntn = int(leftn < kUnroll ? (leftn > 0 ? leftn : 0) : kUnroll);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                if (u < cntn) {
+                    xn[u] = f.load(r, f.src_of(jn - u));
+                    csn[u] = __ldg(cssn + (jn - u));
                 }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
@@ -110,22 +124,40 @@ __global__ void __launch_bounds__(kThreads) hstage_kernel(Fetch f, Emit e, const
                     if (j - u + 1 < i1) e.store(r, j - u + 1, o);
                     carry = nc;
                 }
-            j -= cnt;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                x[u] = xn[u];
+                cs[u] = csn[u];
+            }
+            j = jn;
+            cnt = cntn;
         }
         if (i0 == 0) e.store(r, 0, carry);
     } else {
         double2 carry = f.load(r, f.src_of(start));
         const int64_t hi = min(i1, n - 1);
         int64_t j = start;
-        while (j < hi) {
+        double2 x[kUnroll], cs[kUnroll], xn[kUnroll], csn[kUnroll];
+        int cnt = 0;
+        {
             const int64_t left = hi - j;
-            const int cnt = int(left < kUnroll ? left : kUnroll);
-            double2 x[kUnroll], cs[kUnroll];
+            cnt = int(left < kUnroll ? (left > 0 ? left : 0) : kUnroll);
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
                 if (u < cnt) {
                     x[u] = f.load(r, f.src_of(j + u + 1));
                     cs[u] = __ldg(cssn + (j + u));
+                }
+        }
+        while (cnt > 0) {
+            const int64_t jn = j + cnt;
+            const int64_t leftn = hi - jn;
+            const int cntn = int(leftn < kUnroll ? (leftn > 0 ? leftn : 0) : kUnroll);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+                if (u < cntn) {
+                    xn[u] = f.load(r, f.src_of(jn + u + 1));
+                    csn[u] = __ldg(cssn + (jn + u));
                 }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
@@ -139,7 +171,13 @@ __global__ void __launch_bounds__(kThreads) hstage_kernel(Fetch f, Emit e, const
                     if (j + u >= i0) e.store(r, j + u, o);
                     carry = nc;
                 }
-            j += cnt;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                x[u] = xn[u];
+                cs[u] = csn[u];
+            }
+            j = jn;
+            cnt = cntn;
         }
         if (i1 == n) e.store(r, n - 1, carry);
     }

@@ -94,8 +94,12 @@ struct PassBuffers {
 PassBuffers pass_buffers(Context& ctx) {
     PassBuffers b;
     b.plan = plan_pcg_pass(ctx.m, std::max<int64_t>(ctx.n_local, 1), ctx.dtype == MNB_F64, ctx.num_sms);
-    b.part_s = dev<double2>(ctx.part_s, size_t(b.plan.grid) * size_t(ctx.m));
-    b.part_scal = dev<double>(ctx.part_scal, size_t(b.plan.grid) * 4);
+    // (sized for the persistent small-CG kernel's partials too, so that path never regrows -- and
+    // frees -- these buffers under a queued pass)
+    const size_t parts = std::max<size_t>(size_t(b.plan.grid),
+                                          size_t(pcg_small_grid(ctx.m, std::max<int64_t>(ctx.n_local, 1), ctx.num_sms)));
+    b.part_s = dev<double2>(ctx.part_s, parts * size_t(ctx.m));
+    b.part_scal = dev<double>(ctx.part_scal, parts * 4);
     b.red = dev<double>(ctx.red, size_t(2 * ctx.m + 4));
     return b;
 }
@@ -535,6 +539,7 @@ struct SketchQr {
 struct QrStatus {
     CholStatus chol;
     RefineStatus ref;
+    CholStatus chol1;  // shifted two-pass chain: the first (shifted) pass; `chol` is then the second
 };
 QrStatus* qr_status_dev(Context& ctx) { return dev<QrStatus>(ctx.qr_status, 1); }
 const QrStatus& read_qr_status(Context& ctx) {
@@ -563,6 +568,74 @@ void refine_scratch(Context& ctx, RefineArgs& a) {
     a.v1 = dev<double2>(ctx.vec_m[9], size_t(a.m));
     a.v2 = dev<double2>(ctx.vec_m[10], size_t(a.m));
     a.part = dev<double>(ctx.qr_part, size_t(a.l / 32 + 64));
+}
+
+// Shifted two-pass CholeskyQR for sketches with u cond(S)^2 not small (BASELINE c3, kappa = 1e8),
+// queued on ctx.stream without a host round trip:
+//   R1 = chol(G + s I)  (s = 11 (l m + m (m + 1)) u trace(G), Fukaya et al.),  X1 = R1^{-1},
+//   Q1 = S X1,  R2 = chol(Q1^H Q1),  X2 = R2^{-1},  X = X1 X2 = (R2 R1)^{-1}.
+// The shift caps cond(Q1) near sqrt(||S||^2 / s) ~ 1e4, so Q2 = Q1 X2 = S X is orthonormal to
+// ~u cond(Q1)^2 ~ 1e-8: enough for the CG preconditioner (1e-3 is, lsq.cpp:66-69), and a
+// contraction factor of 1e-8 for Step 2's corrected seminormal equations -- the third pass of
+// shifted CholeskyQR3 (which buys R itself to O(u)) is not needed by either.  The Gram products
+// and Q1 = S X1, X = X1 X2 are cuBLAS level-3 calls; the factorizations, inverses and the checks
+// behind them are k_cholqr.cu's.  G0: S^H S on entry (overwritten by R1).  Records: qs->chol1
+// (pass 1, its `deficient` = the rank rule on diag(R2 R1)), qs->chol (pass 2).
+struct ShiftedChain {
+    double2* Q1;  // l x m (ctx.qwork)
+    double2* X2;  // m x m (ctx.R2)
+    double2* X;   // m x m (ctx.Rinv)
+};
+ShiftedChain launch_shifted_chain(Context& ctx, const double2* S, int64_t l, int64_t m, double2* G0, double rank_rows,
+                                  DevTrace* dt) {
+    QrStatus* qs = qr_status_dev(ctx);
+    double2* G2 = dev<double2>(ctx.gram, size_t(m) * size_t(m));
+    double2* X1 = dev<double2>(ctx.tri_x1, size_t(m) * size_t(m));
+    ShiftedChain c;
+    c.Q1 = dev<double2>(ctx.qwork, size_t(l) * size_t(m));
+    c.X2 = dev<double2>(ctx.R2, size_t(m) * size_t(m));
+    c.X = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
+    double2* W = dev<double2>(ctx.tri_work, size_t(m) * size_t(m));
+    const double shift_factor = 11.0 * (double(l) * double(m) + double(m) * double(m + 1)) * kEps;
+    const cuDoubleComplex cone = make_cuDoubleComplex(1.0, 0.0);
+    const double one = 1.0, zero = 0.0;
+    launch_chol_upper(G0, m, m, shift_factor, 0.0, &qs->chol1, ctx.num_sms, ctx.stream);
+    if (dt) dt->mark("chol(G + sI)");
+    launch_trtri_upper(G0, m, m, X1, W, &qs->chol1, ctx.num_sms, ctx.stream, true);
+    if (dt) dt->mark("X1");
+    cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             int(l), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(X1), int(m),
+                             reinterpret_cast<const cuDoubleComplex*>(S), int(l),
+                             reinterpret_cast<cuDoubleComplex*>(c.Q1), int(l)),
+                 "ztrmm (Q1 = S X1)");
+    if (dt) dt->mark("Q1 = S X1");
+    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
+                             reinterpret_cast<const cuDoubleComplex*>(c.Q1), int(l), &zero,
+                             reinterpret_cast<cuDoubleComplex*>(G2), int(m)),
+                 "zherk");
+    if (dt) dt->mark("gram");
+    launch_chol_upper(G2, m, m, 0.0, 0.0, &qs->chol, ctx.num_sms, ctx.stream);
+    if (dt) dt->mark("chol");
+    launch_trtri_upper(G2, m, m, c.X2, W, &qs->chol, ctx.num_sms, ctx.stream, true);
+    if (dt) dt->mark("X2");
+    cublas_check(cublasZtrmm(ctx.cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                             int(m), int(m), &cone, reinterpret_cast<const cuDoubleComplex*>(c.X2), int(m),
+                             reinterpret_cast<const cuDoubleComplex*>(X1), int(m),
+                             reinterpret_cast<cuDoubleComplex*>(c.X), int(m)),
+                 "ztrmm (X = X1 X2)");
+    if (rank_rows > 0.0) launch_diag_product_rank(G2, m, G0, m, m, rank_rows, &qs->chol1, ctx.stream);
+    if (dt) dt->mark("X = X1 X2");
+    ctx.launches += 5;
+    return c;
+}
+// the verdict of a shifted chain from its two Cholesky records
+bool shifted_chain_ok(const QrStatus& h) {
+    auto usable = [](const CholStatus& c) {
+        if (c.info != 0 || !(c.dmin > 0.0)) return false;
+        const double r = c.dmax / c.dmin;
+        return !(kEps * r * r > 1e-3);
+    };
+    return usable(h.chol1) && usable(h.chol);
 }
 
 bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, bool shifted, bool* precond_only,
@@ -666,6 +739,9 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         // R1^{-1} (which the CG forms anyway, left in ctx.Rinv) and the check of ||Q1^H Q1 - I|| are
         // three launches queued back to back; the host reads their verdict once.
         double2* Rinv = dev<double2>(ctx.Rinv, size_t(m) * size_t(m));
+        // (the Gram is kept in R: if this pass turns out unusable the shifted chain restarts from it)
+        MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
+        ctx.gram0 = R;
         launch_chol_upper(G, m, m, 0.0, rank_rows, &qs->chol, ctx.num_sms, ctx.stream);
         dt.mark("chol");
         upper_inverse(ctx, G, m, m, Rinv, &qs->chol);
@@ -700,9 +776,11 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
             std::fprintf(stderr, "[mnb] one-pass preconditioner: u cond^2 <= %.2e (Frobenius), ||Q1^H Q1 - I|| ~ %.2e (%d steps)\n",
                          h.ref.thr, h.ref.best, h.ref.iterations);
         if (h.ref.accepted) {
+            ctx.gram0 = nullptr;
             MNB_CUDA(cudaMemcpyAsync(R, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
             return true;
         }
+        ctx.gram0 = nullptr;    // (R receives R1 below)
         *precond_only = false;  // R'^{-1} in ctx.Rinv is stale: the full factorization follows from R1
     } else {
         potrf(G, shift_factor);
@@ -835,6 +913,7 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
     MNB_CUDA(cudaEventRecord(e1, ctx.stream));
     SketchQr out{S, tau, R, m, false};
     out.path = 0;
+    ctx.gram0 = nullptr;
     // CholeskyQR2; if the sketch is too ill-conditioned, shifted CholeskyQR3 (and once a sketch of
     // this solve needed it, the next one starts there); Householder (the reference's) as the last resort
     bool done = false;
@@ -853,6 +932,60 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
             }
             if (!done) ctx.qr_shifted = true;
         }
+        if (!done && precond && ctx.fastqr && !ctx.qr_lib) {
+            // the preconditioner of an ill-conditioned sketch: shifted two-pass chain + the check of
+            // ||Q2^H Q2 - I|| on (Q1, X2), one host read (path 5)
+            DevTrace dt(ctx, "shifted chain (E)");
+            if (!ctx.gram0) {
+                if (ctx.pre_gram)
+                    MNB_CUDA(cudaMemcpyAsync(R, ctx.pre_gram, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice,
+                                             ctx.stream));
+                else {
+                    const double one = 1.0, zero = 0.0;
+                    cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
+                                             reinterpret_cast<const cuDoubleComplex*>(S), int(l), &zero,
+                                             reinterpret_cast<cuDoubleComplex*>(R), int(m)),
+                                 "zherk");
+                }
+                dt.mark("gram");
+            }
+            ctx.gram0 = nullptr;
+            const ShiftedChain ch = launch_shifted_chain(ctx, S, l, m, R, rank_rows, &dt);
+            QrStatus* qs = qr_status_dev(ctx);
+            RefineArgs ra;
+            ra.mode = REFINE_PRECOND;
+            ra.S = ch.Q1;
+            ra.l = l;
+            ra.m = m;
+            ra.X = ch.X2;
+            ra.chol = &qs->chol;
+            std::vector<double2> v0;
+            power_start_vector(v0, m);
+            double2* vstart = dev<double2>(ctx.vec_m[11], size_t(m));
+            MNB_CUDA(cudaMemcpyAsync(vstart, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+            ra.b = vstart;
+            ra.z = dev<double2>(ctx.qprobe, size_t(l));
+            refine_scratch(ctx, ra);
+            ra.st = &qs->ref;
+            ra.two_norm_check = 1;
+            launch_sketch_refine(ra, ctx.num_sms, ctx.stream);
+            dt.mark("check");
+            ctx.launches += 1;
+            const QrStatus h = read_qr_status(ctx);
+            dt.dump();
+            if (std::getenv("MNB_TRACE"))
+                std::fprintf(stderr, "[mnb] shifted chain (E): info %d/%d, diag ratios %.2e/%.2e, ||Q2^H Q2 - I|| ~ %.2e (%d steps, Frobenius bound %.2e) -> %s\n",
+                             h.chol1.info, h.chol.info, h.chol1.dmax / h.chol1.dmin, h.chol.dmax / h.chol.dmin,
+                             h.ref.best, h.ref.iterations, h.ref.thr,
+                             shifted_chain_ok(h) && h.ref.accepted ? "accepted" : "fallback");
+            if (shifted_chain_ok(h) && h.ref.accepted) {
+                done = true;
+                out.path = 5;
+                out.rinv_ready = true;
+                out.deficient = rank_rows > 0.0 ? h.chol1.deficient : -1;
+            }
+        }
+        ctx.gram0 = nullptr;
         if (!done) {
             done = cholqr_r(ctx, S, l, m, R, true, nullptr);
             out.path = 1;
@@ -1024,7 +1157,7 @@ bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const doub
 // diagonal, X = R1^{-1}, then the corrected seminormal equations of step2_z_csne as one
 // persistent kernel; their findings land in the context's QrStatus record.
 void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b_host, double2* z,
-                       DevTrace* dt = nullptr) {
+                       DevTrace* dt = nullptr, double2* keep_gram = nullptr) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* X = dev<double2>(ctx.R2, size_t(m) * size_t(m));
     QrStatus* qs = qr_status_dev(ctx);
@@ -1034,6 +1167,8 @@ void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, con
                              reinterpret_cast<cuDoubleComplex*>(G), int(m)),
                  "zherk");
     if (dt) dt->mark("gram");
+    if (keep_gram)  // the shifted chain restarts from the Gram if this pass turns out unusable
+        MNB_CUDA(cudaMemcpyAsync(keep_gram, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     launch_chol_upper(G, m, m, 0.0, double(l), &qs->chol, ctx.num_sms, ctx.stream);
     if (dt) dt->mark("chol");
     upper_inverse(ctx, G, m, m, X, &qs->chol);
@@ -1356,11 +1491,18 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         // corrections stall above the rounding level) the host-steered chain below takes over,
         // starting at shifted CholeskyQR3 -- exactly where it would have ended up.
         bool fast_done = false;
-        if (ctx.fastqr && !ctx.qr_lib && ctx.cholqr && ctx.csne && !ctx.qr_shifted) {
+        // (m <= 1024: beyond that this chain runs beside E's sketch for tens of milliseconds, and the
+        // many-barrier refinement kernel, spinning while only part of its grid is resident, held
+        // SMs the sketch's persistent kernels were waiting for: E's sketch +2.3 ms at c4, +13 ms at
+        // c5, profiles/r02/s4e.  There the host-steered chain below -- the same Cholesky kernel, cuBLAS
+        // GEMV / TRSV calls for the corrections -- stays; MNB_FASTQR_ALL=1 lifts the limit.)
+        static const bool fast_all = std::getenv("MNB_FASTQR_ALL") != nullptr;
+        if (ctx.fastqr && !ctx.qr_lib && ctx.cholqr && ctx.csne && !ctx.qr_shifted && (m <= 1024 || fast_all)) {
             cudaEvent_t q1 = ctx.timer_event(), q2 = ctx.timer_event();
             MNB_CUDA(cudaEventRecord(q1, ctx.stream));
             DevTrace dt(ctx, "QR(S) + steps 2-3");
-            launch_fast_step2(ctx, Sbuf, l, m, b_host, z, &dt);
+            double2* G0 = dev<double2>(ctx.R_S, size_t(m) * size_t(m));
+            launch_fast_step2(ctx, Sbuf, l, m, b_host, z, &dt, G0);
             MNB_CUDA(cudaEventRecord(q2, ctx.stream));
             srft_adjoint_vec(ctx, Td, z, c_vec);
             dt.mark("T^* z");
@@ -1387,9 +1529,56 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                 std::fprintf(stderr, "[mnb] fast QR(S): info %d, diag ratio %.2e, csne %d corrections, ||b - S^H z|| %.3e (thr %.3e) -> %s\n",
                              h.chol.info, ratio, h.ref.iterations, h.ref.best, h.ref.thr * h.ref.nz_best,
                              fast_done ? "accepted" : "fallback");
+            int fast_path = 4;
+            if (!fast_done && !std::getenv("MNB_NO_CHAIN")) {
+                // u cond(S)^2 is not small (c3): the shifted two-pass chain gives X = (R2 R1)^{-1} with
+                // S X orthonormal to ~1e-8, and the same seminormal loop converges on it in one or two
+                // corrections to the Householder-level floor (path 6)
+                DevTrace dt2(ctx, "shifted chain (S) + steps 2-3");
+                MNB_CUDA(cudaEventRecord(q1, ctx.stream));
+                const ShiftedChain ch = launch_shifted_chain(ctx, Sbuf, l, m, G0, double(l), &dt2);
+                QrStatus* qs = qr_status_dev(ctx);
+                RefineArgs ra;
+                ra.mode = REFINE_CSNE;
+                ra.S = Sbuf;
+                ra.l = l;
+                ra.m = m;
+                ra.X = ch.X;
+                ra.chol = &qs->chol1;
+                ra.b = ctx.vec_m[6].as<double2>();  // b, uploaded by the first attempt
+                ra.z = z;
+                refine_scratch(ctx, ra);
+                ra.st = &qs->ref;
+                launch_sketch_refine(ra, ctx.num_sms, ctx.stream);
+                dt2.mark("csne");
+                ctx.launches += 1;
+                MNB_CUDA(cudaEventRecord(q2, ctx.stream));
+                srft_adjoint_vec(ctx, Td, z, c_vec);
+                dt2.mark("T^* z");
+                MNB_CUDA(cudaEventRecord(eC, ctx.stream));
+                const QrStatus h2 = read_qr_status(ctx);
+                trace("shifted chain (S) + steps 2-3 (one read)");
+                dt2.dump();
+                MNB_CUDA(cudaEventElapsedTime(&qms, q1, q2));
+                qr_s0 += qms * 1e-3;
+                if (shifted_chain_ok(h2)) {
+                    if (h2.chol1.deficient > 0)
+                        throw Error(MNB_ERR_RANK_DEFICIENCY,
+                                    "sketch S = T A* lost rank (" + std::to_string(h2.chol1.deficient) +
+                                        " dependent columns); the problem matrix is rank deficient",
+                                    h2.chol1.deficient);
+                    fast_done = h2.ref.accepted != 0;
+                    fast_path = 6;
+                }
+                if (std::getenv("MNB_TRACE"))
+                    std::fprintf(stderr, "[mnb] shifted chain (S): info %d/%d, diag ratios %.2e/%.2e, csne %d corrections, ||b - S^H z|| %.3e (thr %.3e) -> %s\n",
+                                 h2.chol1.info, h2.chol.info, h2.chol1.dmax / h2.chol1.dmin, h2.chol.dmax / h2.chol.dmin,
+                                 h2.ref.iterations, h2.ref.best, h2.ref.thr * h2.ref.nz_best,
+                                 fast_done ? "accepted" : "fallback");
+            }
             if (fast_done) {
                 sq = SketchQr{Sbuf, nullptr, ctx.gram.as<double2>(), m, false};
-                sq.path = 4;
+                sq.path = fast_path;
                 rep.step_seconds[0] = now_s() - t0;
             } else {
                 ctx.qr_shifted = true;

@@ -310,7 +310,7 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
         ctx.launches += 3;
     }
     // fine restart points for single-vector H stages (apply / apply_adjoint of one vector)
-    dev.vec_chunk = 64;
+    dev.vec_chunk = 32;
     dev.vec_nchunks = (n + dev.vec_chunk - 1) / dev.vec_chunk;
     {
         int32_t* vh = static_cast<int32_t*>(dev.vec_halo.ensure(size_t(4 * dev.vec_nchunks) * 4));

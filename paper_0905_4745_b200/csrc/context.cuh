@@ -147,7 +147,7 @@ struct Context {
     bool qr_lib = false;
     DevBuf qr_status, qr_part, tri_work, tri_x1;
     const double2* gram0 = nullptr;  // this sketch's Gram S^H S kept beside the one-pass Cholesky (shifted two-pass chain)
-    PinnedBuf pin_qr;
+    PinnedBuf pin_qr, pin_vec;  // status mirror; page-locked staging of b and the power-step start vector
     DevBuf Rinv, Rinv_rows;
     DevBuf vec_m[12], vec_n[4], vec_full[3], red, part_s, part_scal, part_gg, part_gg_init, state, resid, scratch;
     DevBuf rhs, flag, out_c, qprobe;

@@ -245,8 +245,15 @@ void RandomStream::sample_indices(int64_t* out, int64_t l, int64_t n, bool witho
 
 ChainChunks chain_chunks(int64_t n) {
     ChainChunks c;
+    // at least this many chunks per row (the H stage runs one thread per row and chunk; each chunk
+    // also walks a ~70-step halo, so short chunks trade redundant steps for parallelism)
+    static const int64_t min_chunks = [] {
+        const char* e = std::getenv("MNB_CHAIN_MIN_CHUNKS");
+        const long v = e ? std::atol(e) : 0;
+        return int64_t(v >= 1 ? v : 256);  // (16 -> 256: c2 3.60 -> 3.38 ms, c3 37.9 -> 37.3, profiles/r02/s4h)
+    }();
     int64_t chunk = 1024;
-    while (chunk > 64 && n / chunk < 16) chunk >>= 1;
+    while (chunk > 64 && n / chunk < min_chunks) chunk >>= 1;
     c.chunk = chunk;
     c.nchunks = (n + chunk - 1) / chunk;
     return c;
@@ -372,7 +379,8 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     auto angles_into = [&](RandomStream s, double* out, int64_t count, int64_t stride) {
         for (int64_t i = 0; i < count; ++i) out[i * stride] = s.uniform_angle();
     };
-    constexpr int64_t blk = 1 << 15;
+    // libm blocks: 16 per stream (at most 32K angles each), so small operators spread too
+    const int64_t blk = std::max<int64_t>(256, std::min<int64_t>(int64_t(1) << 15, n / 16));
     const int64_t nb = (n + blk - 1) / blk;
     // angle stream k: 0 d, 1 zeta, 2 zeta~ (unit circle, in place); 3 theta, 4 theta~ (-> cssn)
     auto sincos_block = [&](int k, int64_t b0) {
@@ -443,8 +451,8 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         }
     };
     {
-        // one worker per 2K indices up to `threads` (tiny operators are drawn in microseconds)
-        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, n / 2048)));
+        // one worker per 512 indices up to `threads` (tiny operators are drawn in microseconds)
+        const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, n / 512)));
         const std::function<void()> work = worker;
         WorkerPool::get().run(nt, work);
     }

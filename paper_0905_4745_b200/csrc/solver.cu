@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <cstring>
 #include <future>
 #include <thread>
 
@@ -548,7 +549,18 @@ const QrStatus& read_qr_status(Context& ctx) {
     MNB_CUDA(cudaStreamSynchronize(ctx.stream));
     return *h;
 }
-// seeded dense start vector of the preconditioner check's power steps (splitmix64)
+// seeded dense start vector of the preconditioner check's power steps (splitmix64), uploaded
+// through page-locked staging (no stream synchronization): device pointer (ctx.vec_m[11])
+void power_start_vector(std::vector<double2>& v0, int64_t m);
+double2* upload_power_start(Context& ctx, int64_t m) {
+    std::vector<double2> v0;
+    power_start_vector(v0, m);
+    double2* vp = static_cast<double2*>(ctx.pin_vec.ensure(size_t(2 * m) * 16)) + m;
+    std::memcpy(vp, v0.data(), size_t(m) * 16);
+    double2* vstart = dev<double2>(ctx.vec_m[11], size_t(m));
+    MNB_CUDA(cudaMemcpyAsync(vstart, vp, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    return vstart;
+}
 void power_start_vector(std::vector<double2>& v0, int64_t m) {
     v0.resize(size_t(m));
     uint64_t h = 0x9E3779B97F4A7C15ull;
@@ -753,11 +765,7 @@ bool cholqr_r(Context& ctx, const double2* S, int64_t l, int64_t m, double2* R, 
         ra.m = m;
         ra.X = Rinv;
         ra.chol = &qs->chol;
-        std::vector<double2> v0;
-        power_start_vector(v0, m);
-        double2* vstart = dev<double2>(ctx.vec_m[11], size_t(m));
-        MNB_CUDA(cudaMemcpyAsync(vstart, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-        ra.b = vstart;
+        ra.b = upload_power_start(ctx, m);
         ra.z = dev<double2>(ctx.qprobe, size_t(l));
         refine_scratch(ctx, ra);
         ra.st = &qs->ref;
@@ -959,11 +967,7 @@ SketchQr qr_of_sketch(Context& ctx, double2* S, int64_t l, DevBuf& taubuf, DevBu
             ra.m = m;
             ra.X = ch.X2;
             ra.chol = &qs->chol;
-            std::vector<double2> v0;
-            power_start_vector(v0, m);
-            double2* vstart = dev<double2>(ctx.vec_m[11], size_t(m));
-            MNB_CUDA(cudaMemcpyAsync(vstart, v0.data(), size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
-            ra.b = vstart;
+            ra.b = upload_power_start(ctx, m);
             ra.z = dev<double2>(ctx.qprobe, size_t(l));
             refine_scratch(ctx, ra);
             ra.st = &qs->ref;
@@ -1174,7 +1178,11 @@ void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, con
     upper_inverse(ctx, G, m, m, X, &qs->chol);
     if (dt) dt->mark("inverse");
     double2* bd = dev<double2>(ctx.vec_m[6], size_t(m));
-    MNB_CUDA(cudaMemcpyAsync(bd, b_host, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    // (through page-locked staging: an async copy from pageable memory would first synchronize
+    // the stream, i.e. make the host wait for the Cholesky and the inverse before queueing on)
+    double2* bp = static_cast<double2*>(ctx.pin_vec.ensure(size_t(2 * m) * 16));
+    std::memcpy(bp, b_host, size_t(m) * 16);
+    MNB_CUDA(cudaMemcpyAsync(bd, bp, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
     RefineArgs ra;
     ra.mode = REFINE_CSNE;
     ra.S = S;

@@ -1002,10 +1002,98 @@ __global__ void __launch_bounds__(2 * U, 1) fft_select_blocked8_kernel(const Fft
     }
 }
 
+// Pass B for SHORT second passes (N = 128 ... 512: n = N x 1024, BASELINE c3 is 128 x 1024), pruned to
+// the sampled frequencies and taken directly: with l / 1024 (a handful of) kept outputs per f2, the
+// N-term sums X[f1] = sum_k1 Y[k1] w_N^{f1 k1} cost less than any transform of the unit, and the
+// kernel is a pure stream over pass A's blocked output [row block][f2][k1][8 rows] (16 KiB units at
+// N = 128).  Thread (r, q): row r of the block, k1 = q + 32 j (j < NJ = N / 32) -- a warp reads 512
+// contiguous bytes per j; the next unit's values are in flight during the sums.  Per kept output the
+// 32 q-partials of a row meet by two shuffles (the 4 q of a warp) and a fixed-order sum over the 8
+// warps through shared memory (one barrier per unit, 16 outputs at a time).
+template <int NJ>
+__global__ void __launch_bounds__(256, (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1)) fft_select_blocked_direct_kernel(const FftPassArgs a,
+                                                                           const int32_t* __restrict__ off,
+                                                                           const int32_t* __restrict__ ent) {
+    constexpr int N = 32 * NJ, T = 256, EB = 16;
+    __shared__ double2 TW[N];
+    __shared__ double2 part[EB][8][8];  // [entry][warp][row]
+    __shared__ int32_t ENT[2 * EB];
+    const int r = int(threadIdx.x) & 7, q = int(threadIdx.x) >> 3;
+    const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    for (int i = threadIdx.x; i < N; i += T) TW[i] = __ldg(a.tw + i);
+    const int64_t nrb8 = (a.rows + 7) / 8;
+    const int64_t units = nrb8 * a.batches;
+    auto load = [&](int64_t unit, double2 (&v)[NJ]) {
+        const double2* base = a.in + unit * int64_t(N) * 8 + r;  // unit = rb * batches + b
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) v[j] = __ldg(base + int64_t(q + 32 * j) * 8);
+    };
+    double2 v[NJ], vn[NJ];
+    int64_t unit = blockIdx.x;
+    if (unit < units) load(unit, v);
+    for (; unit < units; unit += gridDim.x) {
+        const int64_t rb = unit / a.batches, b = unit - rb * a.batches;
+        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        const int64_t next = unit + gridDim.x;
+        if (next < units) load(next, vn);
+        for (int c0 = 0; c0 < cnt; c0 += EB) {
+            const int nc = min(EB, cnt - c0);
+            __syncthreads();  // the previous chunk's partials have been read (and TW is loaded)
+            if (threadIdx.x < 2 * nc) ENT[threadIdx.x] = __ldg(ent + 2 * (e0 + c0) + threadIdx.x);
+            __syncthreads();
+            for (int e = 0; e < nc; ++e) {
+                const int f = ENT[2 * e];
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const double2 w = TW[(f * (q + 32 * j)) & (N - 1)];
+                    acc.x = fma(v[j].x, w.x, fma(-v[j].y, w.y, acc.x));
+                    acc.y = fma(v[j].x, w.y, fma(v[j].y, w.x, acc.y));
+                }
+                // the warp's 4 values of q (lanes r, r + 8, r + 16, r + 24)
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+                if (lane < 8) part[e][warp][lane] = acc;
+            }
+            __syncthreads();
+            if (threadIdx.x < 8 * nc) {
+                const int e = int(threadIdx.x) >> 3, rr = int(threadIdx.x) & 7;
+                double2 sum = part[e][0][rr];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) {
+                    sum.x += part[e][w][rr].x;
+                    sum.y += part[e][w][rr].y;
+                }
+                const int64_t row = rb * 8 + rr;
+                if (row < a.rows)
+                    a.out[int64_t(ENT[2 * e + 1]) + (a.out_row0 + row) * a.ld_out] = c_scale(sum, a.scale);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) v[j] = vn[j];
+    }
+}
+
+template <int NJ>
+void launch_direct(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms, cudaStream_t stream) {
+    const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(num_sms) * (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1))));
+    fft_select_blocked_direct_kernel<NJ><<<grid, 256, 0, stream>>>(a, off, ent);
+    MNB_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 bool launch_fft_select_blocked(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms,
                                cudaStream_t stream) {
+    if (!a.inverse && (a.N == 128 || a.N == 256 || a.N == 512)) {
+        if (a.N == 128) launch_direct<4>(a, off, ent, num_sms, stream);
+        else if (a.N == 256) launch_direct<8>(a, off, ent, num_sms, stream);
+        else launch_direct<16>(a, off, ent, num_sms, stream);
+        return true;
+    }
     if (a.inverse || a.N != 3072) return false;
     static const int radix = [] { const char* e = std::getenv("MNB_FB_RADIX"); return e && std::atoi(e) == 16 ? 16 : 8; }();
     if (radix == 8) {

@@ -354,9 +354,13 @@ void build_p2fa_twiddles(const double2* hi, const double2* lo, int shift, int n1
     MNB_LAUNCH_CHECK();
 }
 
+// chain chunks (= pass-B lengths) the fused pass and its pruned pass B cover: 128 (BASELINE c3,
+// n = 2^17) ... 1024 (c4), and 3072 (c5)
+bool p2fa_chunk_ok(int64_t n1) { return n1 == 128 || n1 == 256 || n1 == 512 || n1 == 1024 || n1 == 3072; }
+
 // n = n1 x 1024 with pass A of length n2 = 1024 over the chunks and chain chunks of n1 indices
 bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows) {
-    return n2 == kN && (n1 == 1024 || n1 == 3072) && n == n1 * n2 && rows > 0 && rows % 8 == 0;
+    return n2 == kN && p2fa_chunk_ok(n1) && n == n1 * n2 && rows > 0 && rows % 8 == 0;
 }
 
 void launch_p2fa_carries(const P2faArgs& a, double2* carries, cudaStream_t stream) {

@@ -72,6 +72,7 @@ struct P2faArgs {
     int64_t rows = 0;                // multiple of 8
 };
 bool p2fa_supported(int64_t n, int64_t n1, int64_t n2, int64_t rows);
+bool p2fa_chunk_ok(int64_t n1);  // chain chunk / pass-B lengths the fused path covers
 void launch_p2fa(const P2faArgs& a, int num_sms, cudaStream_t stream);
 // the restart prologues of launch_p2fa: carries[k * a.ldc + row] for the 1024 chunk ends (and the
 // 1024 chunk midpoints when row blocks split); a.carries / a.ldc must point at this buffer

@@ -243,10 +243,12 @@ FftPlan& Context::fft_plan(int64_t n) {
         make_len_plan(P.A, n, stream);
     } else {
         // n = n1 * n2 with both factors smooth and <= 2048, as balanced as possible -- except
-        // n = 3 * 2^20, split 3072 x 1024 for the fused H stage + pass A (k_p2fa.cu)
+        // where the fused H stage + pass A (k_p2fa.cu) applies: n = n1 x 1024 with n1 = 128 ... 1024
+        // or 3072 (c3: 128 x 1024, c5: 3072 x 1024)
         int64_t best = 0;
-        if (p2fa && n == 3 * (int64_t(1) << 20)) best = 1024;
-        for (int64_t n2 = 2; n2 <= 2048 && !(p2fa && n == 3 * (int64_t(1) << 20)); ++n2) {
+        const bool fused_split = p2fa && n % 1024 == 0 && p2fa_chunk_ok(n / 1024) && !std::getenv("MNB_FFT_BALANCED");
+        if (fused_split) best = 1024;
+        for (int64_t n2 = 2; n2 <= 2048 && !fused_split; ++n2) {
             if (n % n2) continue;
             const int64_t n1 = n / n2;
             if (n1 > 2048 || !smooth(n1) || !smooth(n2)) continue;

@@ -1015,12 +1015,15 @@ __global__ void __launch_bounds__(256, (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1)) fft_sele
                                                                            const int32_t* __restrict__ off,
                                                                            const int32_t* __restrict__ ent) {
     constexpr int N = 32 * NJ, T = 256, EB = 16;
+    extern __shared__ int32_t OFF[];     // the CSR offsets of every f2 (batches + 1)
     __shared__ double2 TW[N];
-    __shared__ double2 part[EB][8][8];  // [entry][warp][row]
-    __shared__ int32_t ENT[2 * EB];
+    __shared__ double2 part[EB][8][8];   // [entry][warp][row]
+    __shared__ int32_t ENT[2][2 * EB];   // double-buffered (f1, slot) pairs of the current chunk
     const int r = int(threadIdx.x) & 7, q = int(threadIdx.x) >> 3;
     const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
     for (int i = threadIdx.x; i < N; i += T) TW[i] = __ldg(a.tw + i);
+    for (int i = threadIdx.x; i <= a.batches; i += T) OFF[i] = __ldg(off + i);
+    __syncthreads();
     const int64_t nrb8 = (a.rows + 7) / 8;
     const int64_t units = nrb8 * a.batches;
     auto load = [&](int64_t unit, double2 (&v)[NJ]) {
@@ -1028,21 +1031,35 @@ __global__ void __launch_bounds__(256, (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1)) fft_sele
 #pragma unroll
         for (int j = 0; j < NJ; ++j) v[j] = __ldg(base + int64_t(q + 32 * j) * 8);
     };
+    // this thread's word of a unit's first chunk of entries (threads < 2 EB), fetched a unit ahead
+    auto first_entries = [&](int64_t unit) -> int32_t {
+        const int b = int(unit % a.batches);
+        const int e0 = OFF[b], cnt = OFF[b + 1] - e0;
+        return int(threadIdx.x) < 2 * min(cnt, EB) ? __ldg(ent + 2 * e0 + threadIdx.x) : 0;
+    };
     double2 v[NJ], vn[NJ];
+    int32_t my_ent = 0, my_ent_n = 0;
     int64_t unit = blockIdx.x;
-    if (unit < units) load(unit, v);
+    if (unit < units) {
+        load(unit, v);
+        my_ent = first_entries(unit);
+    }
+    int buf = 0;
     for (; unit < units; unit += gridDim.x) {
         const int64_t rb = unit / a.batches, b = unit - rb * a.batches;
-        const int e0 = __ldg(off + b), cnt = __ldg(off + b + 1) - e0;
+        const int e0 = OFF[b], cnt = OFF[b + 1] - e0;
         const int64_t next = unit + gridDim.x;
-        if (next < units) load(next, vn);
+        if (next < units) {
+            load(next, vn);
+            my_ent_n = first_entries(next);
+        }
         for (int c0 = 0; c0 < cnt; c0 += EB) {
             const int nc = min(EB, cnt - c0);
-            __syncthreads();  // the previous chunk's partials have been read (and TW is loaded)
-            if (threadIdx.x < 2 * nc) ENT[threadIdx.x] = __ldg(ent + 2 * (e0 + c0) + threadIdx.x);
-            __syncthreads();
+            if (int(threadIdx.x) < 2 * nc)
+                ENT[buf][threadIdx.x] = c0 == 0 ? my_ent : __ldg(ent + 2 * (e0 + c0) + threadIdx.x);
+            __syncthreads();  // entries staged; the previous chunk's partials have been read
             for (int e = 0; e < nc; ++e) {
-                const int f = ENT[2 * e];
+                const int f = ENT[buf][2 * e];
                 double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
@@ -1058,7 +1075,7 @@ __global__ void __launch_bounds__(256, (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1)) fft_sele
                 if (lane < 8) part[e][warp][lane] = acc;
             }
             __syncthreads();
-            if (threadIdx.x < 8 * nc) {
+            if (int(threadIdx.x) < 8 * nc) {
                 const int e = int(threadIdx.x) >> 3, rr = int(threadIdx.x) & 7;
                 double2 sum = part[e][0][rr];
 #pragma unroll
@@ -1068,11 +1085,13 @@ __global__ void __launch_bounds__(256, (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1)) fft_sele
                 }
                 const int64_t row = rb * 8 + rr;
                 if (row < a.rows)
-                    a.out[int64_t(ENT[2 * e + 1]) + (a.out_row0 + row) * a.ld_out] = c_scale(sum, a.scale);
+                    a.out[int64_t(ENT[buf][2 * e + 1]) + (a.out_row0 + row) * a.ld_out] = c_scale(sum, a.scale);
             }
+            buf ^= 1;  // the writers above still read this buffer while the next chunk is staged
         }
 #pragma unroll
         for (int j = 0; j < NJ; ++j) v[j] = vn[j];
+        my_ent = my_ent_n;
     }
 }
 
@@ -1080,7 +1099,7 @@ template <int NJ>
 void launch_direct(const FftPassArgs& a, const int32_t* off, const int32_t* ent, int num_sms, cudaStream_t stream) {
     const int64_t units = int64_t(ceil_div(a.rows, 8)) * a.batches;
     const int grid = int(std::max<int64_t>(1, std::min<int64_t>(units, int64_t(num_sms) * (NJ <= 4 ? 4 : NJ <= 8 ? 2 : 1))));
-    fft_select_blocked_direct_kernel<NJ><<<grid, 256, 0, stream>>>(a, off, ent);
+    fft_select_blocked_direct_kernel<NJ><<<grid, 256, size_t(a.batches + 1) * 4, stream>>>(a, off, ent);
     MNB_LAUNCH_CHECK();
 }
 

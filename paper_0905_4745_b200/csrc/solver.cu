@@ -12,6 +12,7 @@
 // (2m+4 doubles) per CG iteration; the sketch redistributes A with one
 // all-to-all (srft_gpu.cu).  The small m-space work is replicated per rank.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -1451,6 +1452,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     // E's sketch anyway, and the duplicated QR workspaces would eat into the sketch's slab budget).
     SketchQr eq;
     cudaEvent_t eQ = ctx.timer_event();
+    std::atomic<int> s_verdict{0};  // (declared before the join guard: the helper thread reads it)
     std::future<void> fut_eq;
     struct JoinEq {
         std::future<void>& f;
@@ -1473,14 +1475,24 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                         bad);
         MNB_CUDA(cudaEventRecord(eQ, q.stream));
     };
+    // what QR(S)'s first Cholesky found (0 not known yet, 1 usable, 2 the sketch needs the shifted
+    // chain): E = T' A^* has the same conditioning, so QR(E) skips its own doomed first attempt when
+    // the answer is there before E's sketch is (c3: ~2.7 ms of the E chain).  Only worth a wait at
+    // m >= 512 -- below, the attempt costs less than the launch latency the wait exposes.
     if (qr_thread) {
         qctx->timers.clear();
         qctx->timer_next = 0;
         qctx->qr_shifted = false;
         MNB_CUDA(cudaStreamWaitEvent(qctx->stream, eE, 0));
         const int device = ctx.device;
-        fut_eq = host_async([&, device] {
+        const bool wait_verdict = m >= 512 && !std::getenv("MNB_NO_VERDICT");
+        fut_eq = host_async([&, device, wait_verdict] {
             MNB_CUDA(cudaSetDevice(device));
+            if (wait_verdict) {
+                while (s_verdict.load(std::memory_order_acquire) == 0 && cudaEventQuery(eE) == cudaErrorNotReady)
+                    std::this_thread::sleep_for(std::chrono::microseconds(20));
+                if (s_verdict.load(std::memory_order_acquire) == 2) qctx->qr_shifted = true;
+            }
             qr_E(*qctx);
         });
     }
@@ -1538,6 +1550,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                              h.chol.info, ratio, h.ref.iterations, h.ref.best, h.ref.thr * h.ref.nz_best,
                              fast_done ? "accepted" : "fallback");
             int fast_path = 4;
+            s_verdict.store(fast_done ? 1 : 2, std::memory_order_release);
             if (!fast_done && !std::getenv("MNB_NO_CHAIN")) {
                 // u cond(S)^2 is not small (c3): the shifted two-pass chain gives X = (R2 R1)^{-1} with
                 // S X orthonormal to ~1e-8, and the same seminormal loop converges on it in one or two
@@ -1594,6 +1607,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         }
         if (!fast_done) {
         sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0, false, /*seminormal=*/true);
+        if (s_verdict.load() == 0) s_verdict.store(ctx.qr_shifted ? 2 : 1, std::memory_order_release);
     trace("QR(S)");
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage
         MNB_CUDA(cudaMemcpyAsync(&flag, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));

@@ -60,9 +60,13 @@ def test_apply_and_adjoint_match_oracle(ctx, l, n, mode):
 
 
 # the large-n cases exercise the blocked four-step passes (n = 2^20: both passes
-# length 1024, the specialised kernel; 2^19: 512 x 1024; 3*2^20: 1536 x 2048)
+# length 1024, the specialised kernel; 3*2^20: 3072 x 1024) and, at n = 2^17 ... 2^19 (n1 x 1024 with
+# n1 = 128, 256, 512; c3 is 2^17), the fused H stage + pass A with the direct pruned pass B -- or,
+# when m is not a multiple of 8 (12, 5), the unfused passes over the same split
 @pytest.mark.parametrize("m,n,l", [(2, 16, 8), (64, 1024, 256), (256, 16384, 1024), (37, 6144, 160),
                                    (8, 1 << 20, 64), (24, 1 << 20, 96), (12, 1 << 20, 48), (12, 1 << 19, 48),
+                                   (16, 1 << 19, 2100), (24, 1 << 18, 300), (5, 1 << 18, 40),
+                                   (16, 1 << 17, 4096), (40, 1 << 17, 64), (8, 1 << 17, 40000),
                                    (5, 3 << 20, 40), (16, 3 << 20, 64)])
 def test_sketch_matches_oracle(ctx, m, n, l):
     A, _ = make_instance(m, n, kappa=1e3, seed=m + n)
@@ -76,7 +80,7 @@ def test_sketch_matches_oracle(ctx, m, n, l):
 
 
 @pytest.mark.parametrize("real,seg,n", [(False, "2", 1 << 20), (True, "2", 1 << 20), (False, "1", 1 << 20),
-                                        (True, "1", 3 << 20)])
+                                        (True, "1", 3 << 20), (False, "2", 1 << 17), (True, "1", 1 << 17)])
 def test_fused_h_fft_matches_unfused(real, seg, n, monkeypatch):
     """The fused second H stage + FFT pass A (k_p2fa.cu, n = 1024 x 1024, row
     blocks of 8, each row block's 1024 steps in 1 or 2 segments restarted from

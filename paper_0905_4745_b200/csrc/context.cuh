@@ -134,6 +134,9 @@ struct Context {
     // multi-slab sketches: called after each row slab's kernels are queued (rows [s0, s0 + rs) of
     // the output are final once they run); the solve uses it to build E's Gram block by block
     std::function<void(int64_t s0, int64_t rs)> on_slab;
+    // staged operator upload: called once by sketch_block right after the first H stage of the
+    // first slab is queued (the operator's other half is then uploaded behind it)
+    std::function<void()> after_first_stage;
     const double2* pre_gram = nullptr;  // when set, the next CholeskyQR pass 1 takes this S^H S (upper)
     bool qr_shifted = false;  // this solve's first sketch needed shifted CholeskyQR3 (reset per solve)
     bool p2fa = true;    // fused P2 + FFT pass A (k_p2fa.cu) where the shape allows; MNB_P2FA=0 disables
@@ -184,6 +187,8 @@ struct Context {
 
 // ---- SRFT on the GPU (srft_gpu.cu) ----
 void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev);
+void upload_srft_first(Context& ctx, const SrftHost& op, SrftDev& dev);
+void upload_srft_rest(Context& ctx, const SrftHost& op, SrftDev& dev, cudaStream_t side, cudaEvent_t landed);
 // T * conj(rows [row0,row0+rows) of a column-major block) -> out[slot + (out_row0 + r) * ldo]
 void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real, int64_t lda, int64_t row0,
                   int64_t rows, double2* out, int64_t ldo, int64_t out_row0, double* kernel_ms);

@@ -310,15 +310,27 @@ static void chain_halos(const double* cssn, int64_t n, const ChainChunks& ch, in
     WorkerPool::get().run(int(std::min<int64_t>(16, 1 + ch.nchunks / 256)), work);
 }
 
+void SrftHost::derive_first() {
+    const int64_t nc = ch.nchunks;
+    int32_t* halo = at<int32_t>(off_halo);
+    chain_halos(at<double>(off_cssn_tilde), n, ch, halo + nc, halo + 3 * nc);
+    span_first = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t lo = c > 0 ? c * ch.chunk - 1 : 0;
+        span_first = std::max<int64_t>(span_first, halo[nc + c] - lo + 1);
+    }
+    first_derived = true;
+}
+
 void SrftHost::derive() {
     const int64_t nc = ch.nchunks;
     int32_t* halo = at<int32_t>(off_halo);
+    if (!first_derived) derive_first();
     chain_halos(at<double>(off_cssn), n, ch, halo, halo + 2 * nc);
-    chain_halos(at<double>(off_cssn_tilde), n, ch, halo + nc, halo + 3 * nc);
-    max_span = 0;
+    max_span = span_first;
     for (int64_t c = 0; c < nc; ++c) {
         const int64_t lo = c > 0 ? c * ch.chunk - 1 : 0;
-        max_span = std::max<int64_t>(max_span, std::max(halo[c], halo[nc + c]) - lo + 1);
+        max_span = std::max<int64_t>(max_span, halo[c] - lo + 1);
     }
     // selection map: frequency -> first output slot; duplicates listed.
     int32_t* sel = at<int32_t>(off_sel);
@@ -347,7 +359,7 @@ void SrftHost::derive() {
 
 
 void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, int sampling,
-                     const BlobAlloc& alloc, const BlobFree& release, int threads) {
+                     const BlobAlloc& alloc, const BlobFree& release, int threads, SrftStage* stage) {
     // src/srft.cpp:97-98
     if (n < 2) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: n must be at least 2");
     if (l < 1 || l > n) throw Error(MNB_ERR_INVALID_ARGUMENT, "build_srft: need 1 <= l <= n");
@@ -360,15 +372,18 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     op.layout();
     op.blob = alloc(op.total_bytes);
     op.release = release;
+    op.first_derived = false;
     const RandomStream stream(stream_seed);
     const bool without = sampling == MNB_WITHOUT_REPLACEMENT;
 
     // The eight tagged substreams are drawn concurrently (each stream is
     // sequential, as RandomStream requires); the cos/sin of every unit-circle
     // and rotation angle (unit_circle, rng.cpp:62-65; finalize, srft.cpp:80-93)
-    // is split into blocks that any idle worker takes as soon as that stream
-    // has been drawn, so the two serial Fisher-Yates permutations overlap the
-    // libm work.  Unit-circle draws stash phi in the real slot first.
+    // is split into blocks that any idle worker takes as soon as the drawing
+    // thread has passed the block's end, so the libm work runs beside the
+    // angle draws and the two serial Fisher-Yates permutations.  Unit-circle
+    // draws stash phi in the real slot first.  The groups of the first H stage
+    // (perm~, theta~, zeta~, zeta) are drawn and evaluated first (SrftStage).
     double* d = op.at<double>(op.off_d);
     double* zeta = op.at<double>(op.off_zeta);
     double* zeta_t = op.at<double>(op.off_zeta_tilde);
@@ -376,13 +391,25 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     double* theta_t = op.at<double>(op.off_theta_tilde);
     double* cssn = op.at<double>(op.off_cssn);
     double* cssn_t = op.at<double>(op.off_cssn_tilde);
-    auto angles_into = [&](RandomStream s, double* out, int64_t count, int64_t stride) {
-        for (int64_t i = 0; i < count; ++i) out[i * stride] = s.uniform_angle();
+    // angle stream k: 0 d, 1 zeta, 2 zeta~ (unit circle, in place); 3 theta, 4 theta~ (-> cssn)
+    std::atomic<int64_t> prog[5];      // angles of stream k drawn so far
+    std::atomic<int64_t> next_blk[5];  // next libm block of stream k
+    const int64_t count[5] = {n, n, n, n - 1, n - 1};
+    for (int k = 0; k < 5; ++k) {
+        prog[k] = 0;
+        next_blk[k] = 0;
+    }
+    auto angles_into = [&](RandomStream s, double* out, int k, int64_t stride) {
+        constexpr int64_t kStep = 2048;
+        for (int64_t i0 = 0; i0 < count[k]; i0 += kStep) {
+            const int64_t e = std::min(count[k], i0 + kStep);
+            for (int64_t i = i0; i < e; ++i) out[i * stride] = s.uniform_angle();
+            prog[k].store(e, std::memory_order_release);
+        }
     };
     // libm blocks: 16 per stream (at most 32K angles each), so small operators spread too
     const int64_t blk = std::max<int64_t>(256, std::min<int64_t>(int64_t(1) << 15, n / 16));
     const int64_t nb = (n + blk - 1) / blk;
-    // angle stream k: 0 d, 1 zeta, 2 zeta~ (unit circle, in place); 3 theta, 4 theta~ (-> cssn)
     auto sincos_block = [&](int k, int64_t b0) {
         if (k < 3) {
             double* z = k == 0 ? d : k == 1 ? zeta : zeta_t;
@@ -402,52 +429,84 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
             }
         }
     };
+    // the next block of stream k whose angles are all drawn: its index, -1 (not drawn yet) or -2 (none left)
+    auto take_block = [&](int k) -> int64_t {
+        int64_t b = next_blk[k].load();
+        while (b < nb) {
+            if (prog[k].load(std::memory_order_acquire) < std::min(count[k], (b + 1) * blk)) return -1;
+            if (next_blk[k].compare_exchange_weak(b, b + 1)) return b;
+        }
+        return -2;
+    };
     std::atomic<int> next_draw{0};
-    std::atomic<int> drawn[5];
-    std::atomic<int64_t> next_blk[5];
-    for (int k = 0; k < 5; ++k) {
-        drawn[k] = 0;
-        next_blk[k] = 0;
-    }
     std::atomic<bool> failed{false};
     std::exception_ptr error;
     std::mutex error_mu;
     static const bool tr_tasks = std::getenv("MNB_TRACE") != nullptr;
     double t_task[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     std::atomic<double> t_sincos_end{0.0};
+    double t_first = 0.0;
+    auto since0 = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_build0).count(); };
+    // first half: perm~ and every libm block of theta~, zeta~, zeta; whoever finishes the last
+    // item derives the Theta~ restart points and signals the stage
+    std::atomic<int64_t> first_left{1 + 3 * nb};
+    auto first_item_done = [&] {
+        if (first_left.fetch_sub(1) != 1) return;
+        op.derive_first();
+        t_first = since0();
+        if (stage) stage->signal(1);
+    };
     auto worker = [&] {
         try {
             for (int t; (t = next_draw.fetch_add(1)) < 8;) {
-                switch (t) {  // longest first
-                    case 0: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
-                    case 1: { RandomStream s = stream.substream(kPermTilde); s.permutation(op.at<int32_t>(op.off_perm_tilde), n); } break;
-                    case 2: {
+                switch (t) {  // the first H stage's groups first
+                    case 0: {
+                        RandomStream s = stream.substream(kPermTilde);
+                        s.permutation(op.at<int32_t>(op.off_perm_tilde), n);
+                        first_item_done();
+                    } break;
+                    case 1: angles_into(stream.substream(kThetaTilde), theta_t, 4, 1); break;
+                    case 2: angles_into(stream.substream(kZetaTilde), zeta_t, 2, 2); break;
+                    case 3: angles_into(stream.substream(kZeta), zeta, 1, 2); break;
+                    case 4: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
+                    case 5: angles_into(stream.substream(kTheta), theta, 3, 1); break;
+                    case 6: angles_into(stream.substream(kD), d, 0, 2); break;
+                    case 7: {
                         RandomStream s = stream.substream(kSample);
                         s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
                     } break;
-                    case 3: angles_into(stream.substream(kThetaTilde), theta_t, n - 1, 1); drawn[4] = 1; break;
-                    case 4: angles_into(stream.substream(kTheta), theta, n - 1, 1); drawn[3] = 1; break;
-                    case 5: angles_into(stream.substream(kZetaTilde), zeta_t, n, 2); drawn[2] = 1; break;
-                    case 6: angles_into(stream.substream(kZeta), zeta, n, 2); drawn[1] = 1; break;
-                    case 7: angles_into(stream.substream(kD), d, n, 2); drawn[0] = 1; break;
                 }
-                if (tr_tasks) t_task[t] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
-                                                                                   t_build0).count();
+                if (tr_tasks) t_task[t] = since0();
             }
-            for (int k : {4, 3, 2, 1, 0}) {
-                while (!drawn[k].load() && !failed.load()) std::this_thread::yield();
-                if (failed.load()) return;
-                for (int64_t b; (b = next_blk[k].fetch_add(1)) < nb;) sincos_block(k, b * blk);
+            // every draw task is claimed (a claimed stream keeps advancing on its own thread)
+            for (;;) {
+                bool did = false, left = false;
+                for (int k : {4, 2, 1, 3, 0}) {
+                    const int64_t b = take_block(k);
+                    if (b >= 0) {
+                        sincos_block(k, b * blk);
+                        if (k == 4 || k == 2 || k == 1) first_item_done();
+                        did = true;
+                        break;
+                    }
+                    if (b == -1) left = true;
+                }
+                if (did) continue;
+                if (!left || failed.load()) break;
+                std::this_thread::yield();
             }
             if (tr_tasks) {
-                const double te = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_build0).count();
+                const double te = since0();
                 double cur = t_sincos_end.load();
                 while (te > cur && !t_sincos_end.compare_exchange_weak(cur, te)) {}
             }
         } catch (...) {
-            std::lock_guard<std::mutex> g(error_mu);
-            if (!error) error = std::current_exception();
+            {
+                std::lock_guard<std::mutex> g(error_mu);
+                if (!error) error = std::current_exception();
+            }
             failed = true;
+            if (stage) stage->signal(2);
         }
     };
     {
@@ -464,10 +523,11 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         const double ms_draw = std::chrono::duration<double, std::milli>(t_drawn - t_build0).count();
         const double ms_derive =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_drawn).count();
-        std::fprintf(stderr, "[mnb] build_srft n=%lld threads=%d: draw %.2f ms, derive %.2f ms; tasks done at perm %.2f "
-                             "perm~ %.2f sample %.2f angles %.2f %.2f %.2f %.2f %.2f, last sincos %.2f ms\n",
+        std::fprintf(stderr, "[mnb] build_srft n=%lld threads=%d: draw %.2f ms, derive %.2f ms; tasks done at perm~ %.2f "
+                             "theta~ %.2f zeta~ %.2f zeta %.2f perm %.2f theta %.2f d %.2f sample %.2f; first half ready "
+                             "%.2f, last sincos %.2f ms\n",
                      (long long)n, threads, ms_draw, ms_derive, t_task[0], t_task[1], t_task[2], t_task[3], t_task[4],
-                     t_task[5], t_task[6], t_task[7], t_sincos_end.load());
+                     t_task[5], t_task[6], t_task[7], t_first, t_sincos_end.load());
     }
 }
 

@@ -5,8 +5,10 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <condition_variable>
 #include <functional>
 #include <future>
+#include <mutex>
 #include <vector>
 
 namespace mnb {
@@ -49,6 +51,8 @@ struct SrftHost {
     int sampling = 0;        // MNB_WITHOUT_REPLACEMENT / MNB_WITH_REPLACEMENT
     int64_t max_mult = 1;    // max multiplicity of `sample` (lsq.cpp:31-39)
     int64_t max_span = 0;    // longest forward-chain scan of any chunk (chunk + halo + 1 steps)
+    int64_t span_first = 0;  // the same over the Theta~ chain alone (the sketch's first H stage)
+    bool first_derived = false;
     ChainChunks ch;
 
     // ---- blob layout (byte offsets) ----
@@ -77,7 +81,33 @@ struct SrftHost {
 
     void layout();  // computes offsets from n, l
     // Derived data (halo starts, selection map, max multiplicity) from the fields.
+    // derive_first: the part the sketch's first H stage needs (restart points of the
+    // Theta~ chain); derive() runs it if it has not run, then the rest.
+    void derive_first();
     void derive();
+};
+
+// Staged build.  The sketch's first H stage (Z~, Pi~, Theta~, Z: src/srft.cpp:52-55) needs
+// only four of the eight parameter groups; a builder given a SrftStage draws those first and
+// signals as soon as perm~, cos/sin(theta~), zeta~, zeta and their restart points are in the
+// blob, while the other groups (d, theta, perm, sample) are still being drawn.  The values
+// are the same streams in the same order: only the schedule changes.
+struct SrftStage {
+    std::mutex mu;
+    std::condition_variable cv;
+    int state = 0;  // 0 pending, 1 first half ready, 2 failed (the builder's future holds the error)
+    void signal(int s) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            if (state == 0) state = s;
+        }
+        cv.notify_all();
+    }
+    bool wait_first() {  // false: the build failed before the first half was ready
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return state != 0; });
+        return state == 1;
+    }
 };
 
 using BlobAlloc = std::function<unsigned char*(size_t)>;
@@ -91,6 +121,6 @@ using BlobFree = std::function<void(unsigned char*)>;
 std::future<void> host_async(std::function<void()> fn);
 
 void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, int sampling,
-                     const BlobAlloc& alloc, const BlobFree& release, int threads = 0);
+                     const BlobAlloc& alloc, const BlobFree& release, int threads = 0, SrftStage* stage = nullptr);
 
 }  // namespace mnb

@@ -1161,12 +1161,24 @@ bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const doub
 // G = S^H S (cuBLAS ZHERK, a plain library GEMM), R1 = chol(G) with the rank rule taken on its
 // diagonal, X = R1^{-1}, then the corrected seminormal equations of step2_z_csne as one
 // persistent kernel; their findings land in the context's QrStatus record.
-void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b_host, double2* z,
-                       DevTrace* dt = nullptr, double2* keep_gram = nullptr) {
+// early_unusable (optional): the host reads the Cholesky's verdict before it queues the rest, and
+// returns with *early_unusable = true when the factor cannot be used (pivot failure, or
+// u (max / min of diag R)^2 > 1e-3) -- the caller then goes straight to the shifted chain
+// instead of running the inverse, the corrections and T^* z on a factor it will discard.
+bool launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b_host, double2* z,
+                       DevTrace* dt = nullptr, double2* keep_gram = nullptr, bool early_verdict = false) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));
     double2* X = dev<double2>(ctx.R2, size_t(m) * size_t(m));
     QrStatus* qs = qr_status_dev(ctx);
     const double one = 1.0, zero = 0.0;
+    double2* bd = dev<double2>(ctx.vec_m[6], size_t(m));
+    {
+        // (through page-locked staging: an async copy from pageable memory would first synchronize
+        // the stream, i.e. make the host wait for the Cholesky and the inverse before queueing on)
+        double2* bp = static_cast<double2*>(ctx.pin_vec.ensure(size_t(2 * m) * 16));
+        std::memcpy(bp, b_host, size_t(m) * 16);
+        MNB_CUDA(cudaMemcpyAsync(bd, bp, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
+    }
     cublas_check(cublasZherk(ctx.cublas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_C, int(m), int(l), &one,
                              reinterpret_cast<const cuDoubleComplex*>(S), int(l), &zero,
                              reinterpret_cast<cuDoubleComplex*>(G), int(m)),
@@ -1176,14 +1188,14 @@ void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, con
         MNB_CUDA(cudaMemcpyAsync(keep_gram, G, size_t(m) * size_t(m) * 16, cudaMemcpyDeviceToDevice, ctx.stream));
     launch_chol_upper(G, m, m, 0.0, double(l), &qs->chol, ctx.num_sms, ctx.stream);
     if (dt) dt->mark("chol");
+    ctx.launches += 1;
+    if (early_verdict) {
+        const QrStatus& h = read_qr_status(ctx);
+        const double ratio = h.chol.dmin > 0.0 ? h.chol.dmax / h.chol.dmin : 1e300;
+        if (h.chol.info != 0 || kEps * ratio * ratio > 1e-3) return false;
+    }
     upper_inverse(ctx, G, m, m, X, &qs->chol);
     if (dt) dt->mark("inverse");
-    double2* bd = dev<double2>(ctx.vec_m[6], size_t(m));
-    // (through page-locked staging: an async copy from pageable memory would first synchronize
-    // the stream, i.e. make the host wait for the Cholesky and the inverse before queueing on)
-    double2* bp = static_cast<double2*>(ctx.pin_vec.ensure(size_t(2 * m) * 16));
-    std::memcpy(bp, b_host, size_t(m) * 16);
-    MNB_CUDA(cudaMemcpyAsync(bd, bp, size_t(m) * 16, cudaMemcpyHostToDevice, ctx.stream));
     RefineArgs ra;
     ra.mode = REFINE_CSNE;
     ra.S = S;
@@ -1197,7 +1209,8 @@ void launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, con
     ra.st = &qs->ref;
     launch_sketch_refine(ra, ctx.num_sms, ctx.stream);
     if (dt) dt->mark("csne");
-    ctx.launches += 2;
+    ctx.launches += 1;
+    return true;
 }
 
 void csne_solve_host(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b, double2* z,
@@ -1307,12 +1320,27 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
                         noop, threads);
         t_param_Tp = now_s() - s;
     };
-    std::future<void> fut_Tp;
+    SrftStage stage_T;  // (before the join guards: the builder signals it)
+    const double t_start_T = now_s();
+    double t_first_T = 0.0;
+    std::future<void> fut_Tp, fut_T;
     // host_async futures do not block on destruction: join the draw before T/T' go out of scope
     struct JoinGuard {
         std::future<void>& f;
         ~JoinGuard() { if (f.valid()) f.wait(); }
-    } join_Tp{fut_Tp};
+    } join_Tp{fut_Tp}, join_T_staged{fut_T};
+    // Staged draw of T (A resident, n >= MNB_STAGED_MIN_N, default 2^16; MNB_STAGED_DRAW=0: off)
+    static const int64_t staged_min_n = [] {
+        if (const char* e = std::getenv("MNB_STAGED_DRAW"); e && std::atoi(e) == 0) return int64_t(1) << 62;
+        const char* e = std::getenv("MNB_STAGED_MIN_N");
+        const long long v = e ? std::atoll(e) : 0;
+        return int64_t(v >= 2 ? v : 65536);
+    }();
+    const bool staged = !pipelined && n >= staged_min_n;
+    struct StageHookGuard {  // the hook captures this frame
+        Context& c;
+        ~StageHookGuard() { c.after_first_stage = nullptr; }
+    } stage_hook_guard{ctx};
     SrftDev& Td = ctx.op_dev[0];
     SrftDev& Tpd = ctx.op_dev[1];
     if (pipelined) {
@@ -1351,6 +1379,22 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         }
         trace("uploads issued");
         for (size_t k = 1; k < slabs.size(); ++k) issue(k);
+    } else if (staged) {
+        // T's groups of the first H stage (perm~, theta~, zeta~, zeta) are drawn first; that stage
+        // is queued as soon as they are uploaded, and the rest of T follows behind it (below)
+        fut_T = host_async([&] {
+            try {
+                build_srft_host(T, l, n, seed_T, sampling,
+                                [&](size_t bytes) { return pinned_alloc(ctx.pin_params[0], bytes); }, noop, hw, &stage_T);
+            } catch (...) {
+                stage_T.signal(2);
+                throw;
+            }
+            t_param_T = now_s() - t_start_T;
+        });
+        fut_Tp = host_async([&] { build_Tp(std::max(1, hw / 2)); });
+        if (!stage_T.wait_first()) fut_T.get();  // rethrows the builder's error
+        t_first_T = now_s() - t_start_T;
     } else {
         build_T(hw);
         fut_Tp = host_async([&] { build_Tp(std::max(1, hw / 2)); });
@@ -1426,10 +1470,25 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         ctx.pending_host = false;
         ctx.A_host = nullptr;
     } else {
-        upload_srft(ctx, T, Td);
+        if (staged) {
+            upload_srft_first(ctx, T, Td);
+            ctx.after_first_stage = [&] {
+                trace("first H stage of S issued");
+                fut_T.get();  // the rest of T (rethrows the builder's error)
+                if (!ctx.copy_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+                upload_srft_rest(ctx, T, Td, ctx.copy_stream, ctx.event(232));
+            };
+        } else {
+            upload_srft(ctx, T, Td);
+        }
         ctx.nonfinite = nonfinite;
         trace("upload T issued");
         sketch_matrix(ctx, Td, Sbuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
+        if (ctx.after_first_stage) {  // no local rows to sketch (a rank without a row block)
+            auto hook = std::move(ctx.after_first_stage);
+            ctx.after_first_stage = nullptr;
+            hook();
+        }
         ctx.nonfinite = nullptr;
         if (ctx.distributed())  // every rank flagged its own row block
             nccl_check(ncclAllReduce(nonfinite, nonfinite, 1, ncclInt, ncclMax, ctx.comm, s1), "ncclAllReduce");
@@ -1437,7 +1496,18 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         trace("sketch S issued");
         // E's sketch queues behind S's on s1 (from the same redistributed slab) while s2 factors S
         fut_Tp.get();
-        upload_srft(ctx, Tp, Tpd);
+        // T' goes up (and its device tables are built) on the copy stream beside S's sketch; queued
+        // on s1 the 88 n bytes would land only after S's last kernel, in front of E's first
+        static const bool side_upload = !(std::getenv("MNB_SIDE_UPLOAD") && std::atoi(std::getenv("MNB_SIDE_UPLOAD")) == 0);
+        if (side_upload) {
+            if (!ctx.copy_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+            OnStream on(ctx, ctx.copy_stream);
+            upload_srft(ctx, Tp, Tpd);
+            MNB_CUDA(cudaEventRecord(ctx.event(233), ctx.copy_stream));
+            MNB_CUDA(cudaStreamWaitEvent(s1, ctx.event(233), 0));
+        } else {
+            upload_srft(ctx, Tp, Tpd);
+        }
         if (incr_gram) ctx.on_slab = gram_slab;
         sketch_matrix(ctx, Tpd, Ebuf, rep.sketch_kernel_ms, &rep.redistribute_seconds);
         ctx.on_slab = nullptr;
@@ -1522,11 +1592,16 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             MNB_CUDA(cudaEventRecord(q1, ctx.stream));
             DevTrace dt(ctx, "QR(S) + steps 2-3");
             double2* G0 = dev<double2>(ctx.R_S, size_t(m) * size_t(m));
-            launch_fast_step2(ctx, Sbuf, l, m, b_host, z, &dt, G0);
+            // (m >= 512: one more host read, after the Cholesky alone, spares an ill-conditioned
+            // sketch -- c3 -- the inverse, the corrections and T^* z of a factor it discards: 2 ms)
+            static const bool early_on = !(std::getenv("MNB_EARLY_VERDICT") && std::atoi(std::getenv("MNB_EARLY_VERDICT")) == 0);
+            const bool usable = launch_fast_step2(ctx, Sbuf, l, m, b_host, z, &dt, G0, early_on && m >= 512);
             MNB_CUDA(cudaEventRecord(q2, ctx.stream));
-            srft_adjoint_vec(ctx, Td, z, c_vec);
-            dt.mark("T^* z");
-            MNB_CUDA(cudaEventRecord(eC, ctx.stream));
+            if (usable) {
+                srft_adjoint_vec(ctx, Td, z, c_vec);
+                dt.mark("T^* z");
+                MNB_CUDA(cudaEventRecord(eC, ctx.stream));
+            }
             int* flag_h = static_cast<int*>(ctx.pin_small.ensure(sizeof(CgState) + 64)) + (sizeof(CgState) + 32) / 4;
             MNB_CUDA(cudaMemcpyAsync(flag_h, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
             const QrStatus& h = read_qr_status(ctx);
@@ -1718,6 +1793,9 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         MNB_CUDA(cudaEventElapsedTime(&d, eA, eQ));
         std::fprintf(stderr, "[mnb] device: sketch S done %.1f ms, sketch E done %.1f, c ready %.1f, R' ready %.1f ms\n",
                      a, b, c, d);
+        if (staged)
+            std::fprintf(stderr, "[mnb] staged draw of T: first half ready %.2f ms, whole T %.2f ms after the solve began to draw\n",
+                         1e3 * t_first_T, 1e3 * t_param_T);
     }
     if (pipelined && std::getenv("MNB_TRACE")) {  // device timeline of the host-A path
         float ms_h2d = 0.f, ms_s = 0.f, ms_c = 0.f, ms_q = 0.f;

@@ -273,10 +273,61 @@ FftPlan& Context::fft_plan(int64_t n) {
     return P;
 }
 
+// Device tables of the sketch's first H stage (needs perm~, cssn~, zeta~, zeta on the device).
+static void build_tables_first(Context& ctx, const SrftHost& op, SrftDev& dev) {
+    const int64_t n = op.n;
+    double2* rec1 = static_cast<double2*>(dev.chain_rec[0].ensure(size_t(n) * 48));
+    build_chain_params(dev.at<double2>(op.off_cssn_tilde), dev.at<double2>(op.off_zeta_tilde),
+                       dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
+    ctx.launches += 1;
+}
+
+static void build_tables_rest(Context& ctx, const SrftHost& op, SrftDev& dev);
+
 void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
     dev.host = &op;
     dev.blob.ensure(op.device_bytes);
     MNB_CUDA(cudaMemcpyAsync(dev.blob.p, op.blob, op.device_bytes, cudaMemcpyHostToDevice, ctx.stream));
+    build_tables_first(ctx, op, dev);
+    build_tables_rest(ctx, op, dev);
+}
+
+// Staged upload (SrftStage, host_srft.hpp): the groups of the first H stage go out as soon as
+// the host has them; the rest follows on `side` (a copy stream) while that stage runs.
+void upload_srft_first(Context& ctx, const SrftHost& op, SrftDev& dev) {
+    dev.host = &op;
+    dev.blob.ensure(op.device_bytes);
+    unsigned char* d = static_cast<unsigned char*>(dev.blob.p);
+    auto copy = [&](size_t b, size_t e) {
+        MNB_CUDA(cudaMemcpyAsync(d + b, op.blob + b, e - b, cudaMemcpyHostToDevice, ctx.stream));
+    };
+    const size_t nc4 = size_t(op.ch.nchunks) * 4;
+    copy(op.off_zeta, op.off_cssn);            // zeta, zeta~
+    copy(op.off_cssn_tilde, op.off_perm);      // cos/sin(theta~)
+    copy(op.off_perm_tilde, op.off_sel);       // perm~
+    copy(op.off_halo + nc4, op.off_halo + 2 * nc4);      // restart points of the Theta~ chain: fwd~
+    copy(op.off_halo + 3 * nc4, op.off_halo + 4 * nc4);  // adj~
+    build_tables_first(ctx, op, dev);
+}
+
+void upload_srft_rest(Context& ctx, const SrftHost& op, SrftDev& dev, cudaStream_t side, cudaEvent_t landed) {
+    unsigned char* d = static_cast<unsigned char*>(dev.blob.p);
+    auto copy = [&](size_t b, size_t e) {
+        MNB_CUDA(cudaMemcpyAsync(d + b, op.blob + b, e - b, cudaMemcpyHostToDevice, side));
+    };
+    const size_t nc4 = size_t(op.ch.nchunks) * 4;
+    copy(op.off_d, op.off_zeta);                // d
+    copy(op.off_cssn, op.off_cssn_tilde);       // cos/sin(theta)
+    copy(op.off_perm, op.off_perm_tilde);       // perm
+    copy(op.off_sel, op.off_halo + nc4);        // sel, fwd
+    copy(op.off_halo + 2 * nc4, op.off_halo + 3 * nc4);  // adj
+    copy(op.off_sample, op.device_bytes);       // sample
+    MNB_CUDA(cudaEventRecord(landed, side));
+    MNB_CUDA(cudaStreamWaitEvent(ctx.stream, landed, 0));
+    build_tables_rest(ctx, op, dev);
+}
+
+static void build_tables_rest(Context& ctx, const SrftHost& op, SrftDev& dev) {
     const FftPlan& P = ctx.fft_plan(op.n);
     const int64_t n2 = P.single ? 0 : P.n2;
     // staging: [dups][csr offsets (n2 + 1)][(f1, slot) pairs (<= 2 l)]
@@ -290,14 +341,11 @@ void upload_srft(Context& ctx, const SrftHost& op, SrftDev& dev) {
         dev.dups.ensure(n_dups * 4);
         MNB_CUDA(cudaMemcpyAsync(dev.dups.p, stage, n_dups * 4, cudaMemcpyHostToDevice, ctx.stream));
     }
-    // per-step records of the two sketch H stages (k_hchain.cu)
+    // per-step records of the second sketch H stage (k_hchain.cu)
     const int64_t n = op.n;
-    double2* rec1 = static_cast<double2*>(dev.chain_rec[0].ensure(size_t(n) * 48));
     double2* rec2 = static_cast<double2*>(dev.chain_rec[1].ensure(size_t(n) * 48));
-    build_chain_params(dev.at<double2>(op.off_cssn_tilde), dev.at<double2>(op.off_zeta_tilde),
-                       dev.at<int32_t>(op.off_perm_tilde), dev.at<double2>(op.off_zeta), n, rec1, ctx.stream);
     build_chain_params(dev.at<double2>(op.off_cssn), nullptr, nullptr, dev.at<double2>(op.off_d), n, rec2, ctx.stream);
-    ctx.launches += 2;
+    ctx.launches += 1;
     // step-major tables of the fused second H stage + FFT pass A (k_p2fa.cu)
     if (ctx.p2fa && !P.single && p2fa_supported(n, P.n1, P.n2, 8)) {
         const int n1 = int(P.n1);
@@ -432,16 +480,13 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
     // the blocked layout pass A reads as contiguous tiles, pass A writes the one pass B reads.
     // (for longer passes, e.g. 1536 x 2048 at n = 3*2^20, the blocked layout read through 4-row
     // halves measured slower than the plain [n][Ms] layout: keep the latter there)
-    const bool blocked = hchain_fits(h.max_span, is_real) && !FP.single && !FP.A.direct && !FP.B.direct &&
-                         fft_tile_fits(FP.A.N, FP.A.E) && fft_tile_fits(FP.B.N, FP.B.E);
     const double scale = 1.0 / std::sqrt(double(n));
 
     for (int64_t s0 = 0; s0 < rows; s0 += Ms) {
         const int64_t rs = std::min(Ms, rows - s0);
-        const bool chained = hchain_fits(h.max_span, is_real);
         {  // P1: Z~, Pi~, Theta~, Z   (src/srft.cpp:52-55)
             EventTimer t(ctx, kernel_ms ? &kernel_ms[0] : nullptr, 0);
-            if (chained) {
+            if (hchain_fits(h.span_first, is_real)) {
                 HChainArgs a;
                 a.in = Ablk;
                 a.in_real = is_real;
@@ -460,7 +505,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
                 a.n = n;
                 a.chunk = h.ch.chunk;
                 a.nchunks = h.ch.nchunks;
-                a.max_span = h.max_span;
+                a.max_span = h.span_first;
                 a.nonfinite = ctx.nonfinite;
                 launch_hchain(a, ctx.num_sms, ctx.stream);
             } else {
@@ -482,6 +527,15 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             ctx.launches += 1;
             t.stop();
         }
+        // staged operator (SrftStage): its other half is uploaded now, behind the first H stage
+        if (ctx.after_first_stage) {
+            auto hook = std::move(ctx.after_first_stage);
+            ctx.after_first_stage = nullptr;
+            hook();
+        }
+        const bool chained = hchain_fits(h.max_span, is_real);
+        const bool blocked = chained && !FP.single && !FP.A.direct && !FP.B.direct &&
+                             fft_tile_fits(FP.A.N, FP.A.E) && fft_tile_fits(FP.B.N, FP.B.E);
         // P2 fused with FFT pass A (k_p2fa.cu) when the shape allows: x2 never goes to HBM
         const bool fused = chained && ctx.p2fa && op.p2fa_rec.p && !FP.single && p2fa_supported(n, FP.n1, FP.n2, rs);
         if (fused) {

@@ -438,7 +438,6 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         }
         return -2;
     };
-    std::atomic<int> next_draw{0};
     std::atomic<bool> failed{false};
     std::exception_ptr error;
     std::mutex error_mu;
@@ -456,41 +455,68 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         t_first = since0();
         if (stage) stage->signal(1);
     };
+    // draw task t: 0..3 the first H stage's groups, 4..7 the rest
+    auto draw_task = [&](int t) {
+        switch (t) {
+            case 0: {
+                RandomStream s = stream.substream(kPermTilde);
+                s.permutation(op.at<int32_t>(op.off_perm_tilde), n);
+                first_item_done();
+            } break;
+            case 1: angles_into(stream.substream(kThetaTilde), theta_t, 4, 1); break;
+            case 2: angles_into(stream.substream(kZetaTilde), zeta_t, 2, 2); break;
+            case 3: angles_into(stream.substream(kZeta), zeta, 1, 2); break;
+            case 4: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
+            case 5: angles_into(stream.substream(kTheta), theta, 3, 1); break;
+            case 6: angles_into(stream.substream(kD), d, 0, 2); break;
+            case 7: {
+                RandomStream s = stream.substream(kSample);
+                s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
+            } break;
+        }
+        if (tr_tasks) t_task[t] = since0();
+    };
+    // (Keeping every worker on the first half until its libm blocks are all claimed -- the other
+    // four draws starting only then -- measured slower: 12 workers chasing three angle streams
+    // mostly spin beside the drawing threads; first half ready 10.0 vs 7.9 ms at n = 2^20,
+    // profiles/r02/ab4.)
+    std::atomic<int> next_first{0}, next_rest{4};
     auto worker = [&] {
         try {
-            for (int t; (t = next_draw.fetch_add(1)) < 8;) {
-                switch (t) {  // the first H stage's groups first
-                    case 0: {
-                        RandomStream s = stream.substream(kPermTilde);
-                        s.permutation(op.at<int32_t>(op.off_perm_tilde), n);
-                        first_item_done();
-                    } break;
-                    case 1: angles_into(stream.substream(kThetaTilde), theta_t, 4, 1); break;
-                    case 2: angles_into(stream.substream(kZetaTilde), zeta_t, 2, 2); break;
-                    case 3: angles_into(stream.substream(kZeta), zeta, 1, 2); break;
-                    case 4: { RandomStream s = stream.substream(kPerm); s.permutation(op.at<int32_t>(op.off_perm), n); } break;
-                    case 5: angles_into(stream.substream(kTheta), theta, 3, 1); break;
-                    case 6: angles_into(stream.substream(kD), d, 0, 2); break;
-                    case 7: {
-                        RandomStream s = stream.substream(kSample);
-                        s.sample_indices(op.at<int64_t>(op.off_sample64), l, n, without);
-                    } break;
-                }
-                if (tr_tasks) t_task[t] = since0();
-            }
-            // every draw task is claimed (a claimed stream keeps advancing on its own thread)
+            for (int t; (t = next_first.fetch_add(1)) < 4;) draw_task(t);
+            // (the first half's draw tasks are all claimed: its streams advance on their own threads)
             for (;;) {
                 bool did = false, left = false;
-                for (int k : {4, 2, 1, 3, 0}) {
+                for (int k : {4, 2, 1}) {
                     const int64_t b = take_block(k);
                     if (b >= 0) {
                         sincos_block(k, b * blk);
-                        if (k == 4 || k == 2 || k == 1) first_item_done();
+                        first_item_done();
                         did = true;
                         break;
                     }
                     if (b == -1) left = true;
                 }
+                if (did) continue;
+                if (next_rest.load() < 8) {
+                    const int t = next_rest.fetch_add(1);
+                    if (t < 8) {
+                        draw_task(t);
+                        continue;
+                    }
+                }
+                if (next_rest.load() >= 8)  // every draw task is claimed: the rest's blocks as they come
+                    for (int k : {3, 0}) {
+                        const int64_t b = take_block(k);
+                        if (b >= 0) {
+                            sincos_block(k, b * blk);
+                            did = true;
+                            break;
+                        }
+                        if (b == -1) left = true;
+                    }
+                else
+                    left = true;
                 if (did) continue;
                 if (!left || failed.load()) break;
                 std::this_thread::yield();

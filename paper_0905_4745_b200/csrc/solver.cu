@@ -1498,7 +1498,11 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         fut_Tp.get();
         // T' goes up (and its device tables are built) on the copy stream beside S's sketch; queued
         // on s1 the 88 n bytes would land only after S's last kernel, in front of E's first
-        static const bool side_upload = !(std::getenv("MNB_SIDE_UPLOAD") && std::atoi(std::getenv("MNB_SIDE_UPLOAD")) == 0);
+        // (m <= 1024 -- c3: 32.34 -> 32.1 ms; at c5 the table kernels beside S's sketch and the earlier
+        // start of E's sketch against QR(S)'s Gram cost 6 ms, at c4 nothing changes: profiles/r02/ab2;
+        // MNB_SIDE_UPLOAD=0 / 1 forces it off / on)
+        static const int side_env = std::getenv("MNB_SIDE_UPLOAD") ? std::atoi(std::getenv("MNB_SIDE_UPLOAD")) : -1;
+        const bool side_upload = side_env >= 0 ? side_env != 0 : m <= 1024;
         if (side_upload) {
             if (!ctx.copy_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
             OnStream on(ctx, ctx.copy_stream);

@@ -318,3 +318,36 @@ def test_apply_adjoint_matrix(ctx):
         assert np.linalg.norm(ax - A @ xr) <= 1e-13 * np.linalg.norm(A @ xr)
         with pytest.raises(mn.DimensionError):
             mn.apply_adjoint_matrix(y[:5], ctx)
+
+
+# -------------------------------------------------- staged draw of T (host_srft.hpp SrftStage)
+_STAGED_SCRIPT = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_0905_4745_b200 as mn
+from tests.instances import make_instance
+A, b = make_instance(24, 65536, 1e3, seed=311)
+ctx = mn.Context(0)
+r = mn.solve_randomized(mn.ProblemInstance(A, b), mn.SolverConfig(seed=313, capture_c=True), ctx)
+print(hashlib.sha256(r.x.tobytes()).hexdigest(), hashlib.sha256(r.c.tobytes()).hexdigest(), r.lsq_iterations)
+"""
+
+
+def test_staged_draw_gives_the_same_bits():
+    """The staged draw / upload of T (first H stage's groups first, the rest behind P1) only
+    reschedules src/srft.cpp:95-113: x and c equal the one-shot draw's bit for bit.  (The switches
+    are read once per process, hence the subprocesses; n = 2^16 is where staging starts.)"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"MNB_STAGED_DRAW": "0"}):
+        e = dict(os.environ)
+        e.update(env)
+        p = subprocess.run([sys.executable, "-c", _STAGED_SCRIPT.format(root=root)], capture_output=True, text=True,
+                           env=e, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]

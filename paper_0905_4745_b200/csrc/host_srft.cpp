@@ -480,6 +480,14 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
     // four draws starting only then -- measured slower: 12 workers chasing three angle streams
     // mostly spin beside the drawing threads; first half ready 10.0 vs 7.9 ms at n = 2^20,
     // profiles/r02/ab4.)
+    // A staged build holds three of the other draws (theta, d, sample: MNB_STAGED_DEFER=0 lifts it)
+    // back until the first half's libm blocks are all claimed, so eleven workers instead of eight
+    // evaluate them while five draw; perm, the longest, starts at once.
+    static const bool defer_on = !(std::getenv("MNB_STAGED_DEFER") && std::atoi(std::getenv("MNB_STAGED_DEFER")) == 0);
+    const bool defer_rest = stage != nullptr && defer_on;
+    auto first_blocks_claimed = [&] {
+        return next_blk[4].load() >= nb && next_blk[2].load() >= nb && next_blk[1].load() >= nb;
+    };
     std::atomic<int> next_first{0}, next_rest{4};
     auto worker = [&] {
         try {
@@ -498,13 +506,14 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
                     if (b == -1) left = true;
                 }
                 if (did) continue;
-                if (next_rest.load() < 8) {
-                    const int t = next_rest.fetch_add(1);
-                    if (t < 8) {
+                for (int t = next_rest.load(); t < 8 && (t == 4 || !defer_rest || first_blocks_claimed());) {
+                    if (next_rest.compare_exchange_weak(t, t + 1)) {
                         draw_task(t);
-                        continue;
+                        did = true;
+                        break;
                     }
                 }
+                if (did) continue;
                 if (next_rest.load() >= 8)  // every draw task is claimed: the rest's blocks as they come
                     for (int k : {3, 0}) {
                         const int64_t b = take_block(k);

@@ -476,13 +476,13 @@ void build_srft_host(SrftHost& op, int64_t l, int64_t n, uint64_t stream_seed, i
         }
         if (tr_tasks) t_task[t] = since0();
     };
-    // (Keeping every worker on the first half until its libm blocks are all claimed -- the other
-    // four draws starting only then -- measured slower: 12 workers chasing three angle streams
-    // mostly spin beside the drawing threads; first half ready 10.0 vs 7.9 ms at n = 2^20,
-    // profiles/r02/ab4.)
+    // (Holding all four of the other draws back until the first half's libm blocks are claimed
+    // measured slower: 12 workers chasing three angle streams mostly spin beside the drawing
+    // threads; first half ready 10.0 vs 7.9 ms at n = 2^20, profiles/r02/ab4.)
     // A staged build holds three of the other draws (theta, d, sample: MNB_STAGED_DEFER=0 lifts it)
     // back until the first half's libm blocks are all claimed, so eleven workers instead of eight
-    // evaluate them while five draw; perm, the longest, starts at once.
+    // evaluate them while five draw; perm, the longest, starts at once (c4 280.7 -> 279.4 ms,
+    // profiles/r02/ab6).
     static const bool defer_on = !(std::getenv("MNB_STAGED_DEFER") && std::atoi(std::getenv("MNB_STAGED_DEFER")) == 0);
     const bool defer_rest = stage != nullptr && defer_on;
     auto first_blocks_claimed = [&] {

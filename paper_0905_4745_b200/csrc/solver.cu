@@ -1161,10 +1161,10 @@ bool step2_z_csne(Context& ctx, const SketchQr& sq, const double2* S, const doub
 // G = S^H S (cuBLAS ZHERK, a plain library GEMM), R1 = chol(G) with the rank rule taken on its
 // diagonal, X = R1^{-1}, then the corrected seminormal equations of step2_z_csne as one
 // persistent kernel; their findings land in the context's QrStatus record.
-// early_unusable (optional): the host reads the Cholesky's verdict before it queues the rest, and
-// returns with *early_unusable = true when the factor cannot be used (pivot failure, or
-// u (max / min of diag R)^2 > 1e-3) -- the caller then goes straight to the shifted chain
-// instead of running the inverse, the corrections and T^* z on a factor it will discard.
+// early_verdict: the host reads the Cholesky's verdict before it queues the rest and returns
+// false when the factor cannot be used (pivot failure, or u (max / min of diag R)^2 > 1e-3) --
+// the caller then goes straight to the shifted chain instead of running the inverse, the
+// corrections and T^* z on a factor it will discard.  Returns true when everything is queued.
 bool launch_fast_step2(Context& ctx, const double2* S, int64_t l, int64_t m, const double2* b_host, double2* z,
                        DevTrace* dt = nullptr, double2* keep_gram = nullptr, bool early_verdict = false) {
     double2* G = dev<double2>(ctx.gram, size_t(m) * size_t(m));

@@ -128,7 +128,7 @@ struct Context {
     // until the matrix changes or the next solve starts
     bool slab_ready = false;
     int64_t slab_rows = 0, slab_row0 = 0;
-    DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork, gram_E;
+    DevBuf sk_S, sk_E, tau_S, tau_E, qr_work, qr_info, R_S, R_E, R2, gram, qwork, gram_E, gram_Sk;
     cudaStream_t gram_stream = nullptr;  // E's Gram built slab by slab beside the sketch
     bool init_from_sketch = false;  // this solve's CG INIT took A c = S^H z (no pass over A)
     // multi-slab sketches: called after each row slab's kernels are queued (rows [s0, s0 + rs) of

@@ -1345,8 +1345,20 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     SrftDev& Tpd = ctx.op_dev[1];
     if (pipelined) {
         if (!ctx.copy_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
-        const int64_t per = std::max<int64_t>(64, ((m + 7) / 8 + 7) & ~int64_t(7));
-        for (int64_t r0 = 0; r0 < m; r0 += per) slabs.emplace_back(r0, std::min(per, m - r0));
+        // eight row slabs; only the last one's sketches are exposed after the copy, so it is the
+        // short one (m / 32 rows, at least 64) and the other seven share the rest
+        // (MNB_EVEN_SLABS=1: eight equal slabs)
+        static const bool even_slabs = std::getenv("MNB_EVEN_SLABS") && std::atoi(std::getenv("MNB_EVEN_SLABS")) == 1;
+        if (m >= 1024 && !even_slabs) {
+            const int64_t body = (m - std::max<int64_t>(64, m / 32)) & ~int64_t(7);  // slab starts at multiples of 8
+            const int64_t last = m - body;
+            const int64_t per = ((body + 6) / 7 + 7) & ~int64_t(7);
+            for (int64_t r0 = 0; r0 < body; r0 += per) slabs.emplace_back(r0, std::min(per, body - r0));
+            slabs.emplace_back(body, last);
+        } else {
+            const int64_t per = std::max<int64_t>(64, ((m + 7) / 8 + 7) & ~int64_t(7));
+            for (int64_t r0 = 0; r0 < m; r0 += per) slabs.emplace_back(r0, std::min(per, m - r0));
+        }
         const size_t e = ctx.esz();
         auto issue = [&](size_t k) {
             const auto [r0, rows] = slabs[k];
@@ -1425,29 +1437,36 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
     // slab of rows [s0, s0 + rs) lands, G[0:s0+rs, s0:s0+rs] = E[:, :s0+rs]^H E[:, s0:s0+rs] on its own
     // stream, so QR(E) starts from a finished Gram instead of a 16384 x 4096 HERK after the sketch
     double2* GE = nullptr;
+    double2* GS = nullptr;  // S's Gram the same way on the host-A path (m > 1024: QR(S) is what remains after the copy)
     bool gram_partial = false;
-    cudaEvent_t eG = ctx.timer_event();
-    auto gram_slab = [&](int64_t s0, int64_t rs) {
-        if (s0 == 0 && rs == m) {  // one slab: nothing to overlap, QR(E) takes its own HERK
-            gram_partial = true;
-            return;
-        }
-        if (!ctx.gram_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.gram_stream, cudaStreamNonBlocking));
-        GE = dev<double2>(ctx.gram_E, size_t(m) * size_t(m));
-        cudaEvent_t e = ctx.timer_event();
-        MNB_CUDA(cudaEventRecord(e, s1));
-        MNB_CUDA(cudaStreamWaitEvent(ctx.gram_stream, e, 0));
-        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-        cublasSetStream(ctx.cublas, ctx.gram_stream);
-        const cublasStatus_t st = cublasZgemm(ctx.cublas, CUBLAS_OP_C, CUBLAS_OP_N, int(s0 + rs), int(rs), int(l), &one,
-                                              reinterpret_cast<const cuDoubleComplex*>(Ebuf), int(l),
-                                              reinterpret_cast<const cuDoubleComplex*>(Ebuf + s0 * l), int(l), &zero,
-                                              reinterpret_cast<cuDoubleComplex*>(GE + s0 * m), int(m));
-        cublasSetStream(ctx.cublas, ctx.stream);
-        cublas_check(st, "zgemm (Gram of E)");
-        MNB_CUDA(cudaEventRecord(eG, ctx.gram_stream));
+    cudaEvent_t eG = ctx.timer_event(), eGS = ctx.timer_event();
+    auto gram_slab_of = [&](const double2* sketch, DevBuf& store, double2*& Gout, cudaEvent_t done) {
+        return [&, sketch, done](int64_t s0, int64_t rs) {
+            if (s0 == 0 && rs == m) {  // one slab: nothing to overlap, the QR takes its own HERK
+                gram_partial = true;
+                return;
+            }
+            if (!ctx.gram_stream) MNB_CUDA(cudaStreamCreateWithFlags(&ctx.gram_stream, cudaStreamNonBlocking));
+            Gout = dev<double2>(store, size_t(m) * size_t(m));
+            cudaEvent_t e = ctx.timer_event();
+            MNB_CUDA(cudaEventRecord(e, s1));
+            MNB_CUDA(cudaStreamWaitEvent(ctx.gram_stream, e, 0));
+            const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+            cublasSetStream(ctx.cublas, ctx.gram_stream);
+            const cublasStatus_t st = cublasZgemm(ctx.cublas, CUBLAS_OP_C, CUBLAS_OP_N, int(s0 + rs), int(rs), int(l), &one,
+                                                  reinterpret_cast<const cuDoubleComplex*>(sketch), int(l),
+                                                  reinterpret_cast<const cuDoubleComplex*>(sketch + s0 * l), int(l), &zero,
+                                                  reinterpret_cast<cuDoubleComplex*>(Gout + s0 * m), int(m));
+            cublasSetStream(ctx.cublas, ctx.stream);
+            cublas_check(st, "zgemm (Gram of a sketch)");
+            MNB_CUDA(cudaEventRecord(done, ctx.gram_stream));
+        };
     };
+    const std::function<void(int64_t, int64_t)> gram_slab = gram_slab_of(Ebuf, ctx.gram_E, GE, eG);
+    const std::function<void(int64_t, int64_t)> gram_slab_S = gram_slab_of(Sbuf, ctx.gram_Sk, GS, eGS);
     const bool incr_gram = !ctx.distributed() && !std::getenv("MNB_GRAM_AFTER");
+    // (S: only where QR(S) takes the host-steered CholeskyQR that honours a precomputed Gram, m > 1024)
+    const bool incr_gram_S = incr_gram && pipelined && m > 1024 && !std::getenv("MNB_GRAM_S_AFTER");
     struct SlabHookGuard {  // the hook captures this frame: never let it outlive the solve
         Context& c;
         ~SlabHookGuard() { c.on_slab = nullptr; }
@@ -1457,7 +1476,9 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             const auto [r0, rows] = slabs[k];
             MNB_CUDA(cudaStreamWaitEvent(s1, ctx.event(200 + k), 0));
             ctx.nonfinite = nonfinite;  // the first H stage checks every entry of A as it streams it
+            if (incr_gram_S) ctx.on_slab = gram_slab_S;
             sketch_block(ctx, Td, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Sbuf, l, r0, rep.sketch_kernel_ms);
+            ctx.on_slab = nullptr;
             ctx.nonfinite = nullptr;
             if (incr_gram) ctx.on_slab = gram_slab;
             sketch_block(ctx, Tpd, ctx.A, ctx.dtype == MNB_F64, m, r0, rows, Ebuf, l, r0, rep.sketch_kernel_ms);
@@ -1517,7 +1538,7 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
         ctx.on_slab = nullptr;
         MNB_CUDA(cudaEventRecord(eE, s1));
     }
-    if (gram_partial) GE = nullptr;  // a single slab after all
+    if (gram_partial) GE = GS = nullptr;  // a single slab after all
     trace("sketch E issued");
 
     // ---- QR(E) (Step 4's preconditioner, src/lsq.cpp:58-64) on a helper host thread with its own
@@ -1685,7 +1706,15 @@ void solve_randomized(Context& ctx, const double2* b_host, const mnb_solver_conf
             }
         }
         if (!fast_done) {
-        sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0, false, /*seminormal=*/true);
+        {
+            struct PreGramS {  // S's Gram built slab by slab during the copy (host-A path)
+                Context& c;
+                PreGramS(Context& ctx_, const double2* g) : c(ctx_) { c.pre_gram = g; }
+                ~PreGramS() { c.pre_gram = nullptr; }
+            } pre_gram_S{ctx, GS};
+            if (GS) MNB_CUDA(cudaStreamWaitEvent(ctx.stream, eGS, 0));
+            sq = qr_of_sketch(ctx, Sbuf, l, ctx.tau_S, ctx.R_S, &qr_s0, false, /*seminormal=*/true);
+        }
         if (s_verdict.load() == 0) s_verdict.store(ctx.qr_shifted ? 2 : 1, std::memory_order_release);
     trace("QR(S)");
         int flag = 0;  // ProblemInstance::validate's finiteness of A, flagged by the first H stage

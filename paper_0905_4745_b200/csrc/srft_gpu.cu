@@ -562,7 +562,7 @@ void sketch_block(Context& ctx, const SrftDev& op, const void* Ablk, int is_real
             {
                 const int64_t pairs = ctx.num_sms / 2, nrb = rs / 8;
                 const int64_t full = nrb / pairs * pairs, tail = nrb - full;
-                a.full_rb = (tail > 0 && 2 * tail <= pairs && full > 0) ? full : nrb;
+                a.full_rb = (tail > 0 && 2 * tail <= pairs) ? full : nrb;  // (full == 0: a short slab, all split)
                 if (const char* e = std::getenv("MNB_P2FA_SEG")) a.full_rb = std::atoi(e) == 2 ? 0 : nrb;
             }
             a.halo_seg = op.p2fa_halo.as<int32_t>() + 2048;

@@ -207,25 +207,31 @@ def test_lsq_fixed_seed_is_bitwise_reproducible(ctx):
     assert y1.tobytes() == y2.tobytes()
 
 
-def test_pinned_host_matrix_pipelined_copy_matches(ctx):
+@pytest.mark.parametrize("m,n", [(192, 4096), (1032, 8192)])
+def test_pinned_host_matrix_pipelined_copy_matches(ctx, m, n):
     """A page-locked host A takes the MNB_HOST_ASYNC path (row-slab H2D overlapped with both
-    sketches); the solve must equal the one from a pageable (eagerly copied) A."""
+    sketches); the solve must equal the one from a pageable (eagerly copied) A.  (m >= 1024:
+    seven equal slabs and a short, here ragged, last one.)"""
     torch = pytest.importorskip("torch")
-    A, b = make_instance(192, 4096, 1e3, seed=113)
+    A, b = make_instance(m, n, 1e3, seed=113)
     pinned = torch.empty((A.shape[1], A.shape[0]), dtype=torch.complex128, pin_memory=True)
     pinned.copy_(torch.from_numpy(np.ascontiguousarray(A.T)))
     A_pinned = pinned.numpy().T  # column-major view of page-locked memory
     cfg = mn.SolverConfig(epsilon=1e-10, capture_c=True)
     r_pin = mn.solve_randomized(mn.ProblemInstance(A_pinned, b), cfg, ctx)
     r_page = mn.solve_randomized(mn.ProblemInstance(np.asfortranarray(A), b), cfg, ctx)
-    # the sketches and c are bit-identical; the pipelined path forms E's Gram block by block as the
-    # slabs land (one ZGEMM per slab) where the eager path takes one ZHERK, so R' -- and the CG
-    # iterates -- agree to rounding
-    assert r_pin.c.tobytes() == r_page.c.tobytes()
+    # the sketches are bit-identical; the pipelined path forms E's Gram block by block as the slabs
+    # land (one ZGEMM per slab) where the eager path takes one ZHERK, so R' -- and the CG iterates --
+    # agree to rounding.  For m > 1024 it forms S's Gram the same way, so there c agrees to rounding
+    # too; below that QR(S) takes its own ZHERK and c is bit-identical.
+    if m <= 1024:
+        assert r_pin.c.tobytes() == r_page.c.tobytes()
+    else:
+        assert np.linalg.norm(r_pin.c - r_page.c) <= 1e-12 * np.linalg.norm(r_page.c)
     assert r_pin.lsq_iterations == r_page.lsq_iterations
     assert np.linalg.norm(r_pin.x - r_page.x) <= 1e-12 * np.linalg.norm(r_page.x)
     # a later call on the same context sees the resident matrix
-    op = mn.build_srft(4 * 192, 4096, mn.derive_seed(42, 11))
+    op = mn.build_srft(4 * m, n, mn.derive_seed(42, 11))
     ctx.set_matrix(A_pinned, deferred=True)
     S1 = op.sketch(ctx)
     ctx.set_matrix(np.asfortranarray(A))
